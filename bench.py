@@ -1,0 +1,396 @@
+"""Benchmark: FCM voxel-iterations/s on B200, BASELINE config 4 (512^3, c=3, m=2).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl ours|reference]
+
+One STEP = one complete solve, i.e. one fcm_run: the device-side seeded start
+(prologue: u_0 sums -> v_1) plus every fused pass until max|u_k - u_{k-1}| <
+epsilon -- exactly the region the reference harness times around _iterate
+(reference bench.py:49-59).  value = voxels x iterations / time, inputs
+resident in HBM.  `e2e` times the same solve through the C ABI from host
+buffers: pixel upload (uint8), solve, and download of the final membership
+(AoS float64) and labels.
+
+N > 1 (torchrun, one process per GPU): each rank owns a contiguous,
+tile-aligned voxel shard; the only per-iteration exchange is an
+ncclAllGather of the 2c+2 reduction roots (64 B at c=3) -- weak sharding of a
+fixed problem, reported as "strong" scaling (total work fixed).
+
+--impl reference runs the reference's own CPU engine (fcmseg from oracle/_ref,
+parallel._iterate on all host threads; the oracle port when oracle/_ref is
+absent) on a bounded slab of the same volume.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+CONFIGS = {
+    # name: (shape (nz, ny, nx), c, m, epsilon)
+    "C4": ((512, 512, 512), 3, 2.0, 1e-5),
+    "C2": ((181, 217, 181), 3, 2.0, 1e-5),
+    "C5": ((512, 1024, 1024), 8, 1.5, 1e-5),
+}
+BYTES_PER_VOXEL_ITER = {3: 25, 8: 65}  # x (u8) + read u_{k-1} fp32 SoA + write u_k
+
+
+def algorithmic_bytes(c: int) -> int:
+    return 1 + 8 * c
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def load_traffic(config: str):
+    """Per-launch dram bytes of the pass kernel from the committed ncu summary, if any."""
+    p = os.path.join(REPO, "profiles", f"ncu_pass_{config}.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["dram_bytes_per_launch"])
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, smax, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[2:6]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(smax), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def make_volume(shape, rank_slice=None):
+    from paper_1601_00072_b200.phantom import phantom_slice
+    nz, ny, nx = shape
+    vol = np.empty((nz, ny, nx), dtype=np.uint8)
+    for z in range(nz):
+        vol[z] = phantom_slice(nx, ny, (z - nz / 2) / nz, seed=5 * 100003 + z)
+    return vol.reshape(-1)
+
+
+# --------------------------------------------------------------- CPU legs --
+def cpu_reference_sample(shape, c, m, eps, slab=32, iters=3):
+    """Reference CPU engine on a slab of the same volume: voxel-iter/s, kind, cores, sample."""
+    from paper_1601_00072_b200.phantom import phantom_slice
+    nz, ny, nx = shape
+    z0 = nz // 2 - slab // 2
+    x = np.stack([phantom_slice(nx, ny, (z - nz / 2) / nz, seed=5 * 100003 + z) for z in range(z0, z0 + slab)])
+    x = x.reshape(-1).astype(np.float64)
+    n = x.shape[0]
+    cores = os.cpu_count() or 1
+    sample = f"{slab}-slice slab ({nx}x{ny}x{slab} = {n} voxels) of the same phantom, max_iters={iters}"
+    try:
+        sys.path.insert(0, os.path.join(REPO, "oracle", "_ref"))
+        import fcmseg
+        from fcmseg import core, parallel
+        assert fcmseg.backend_name() == "compiled"
+        cfg = fcmseg.FcmConfig(c=c, m=m, epsilon=eps, max_iters=iters, seed=0)
+        u0 = core.init_membership(n, cfg).u
+        t0 = time.perf_counter()
+        _, _, k, _, _, _ = parallel._iterate(x, u0.copy(), cfg, cores)
+        dt = time.perf_counter() - t0
+        kind = "reference"
+        sample += "; fcmseg parallel._iterate (compiled Cython kernels), workers=os.cpu_count()"
+    except Exception as e:  # oracle/_ref not built on this box: the C restatement
+        from oracle import oracle as O
+        u0 = O.fill_membership_random(n, c, 0)
+        t0 = time.perf_counter()
+        _, _, k, _, _ = O.iterate(x, u0, c, m, eps, iters, engine="parallel")
+        dt = time.perf_counter() - t0
+        kind = "port"
+        sample += f"; oracle port iterate_parallel (OpenMP), reference unavailable: {type(e).__name__}"
+    return n * k / dt, kind, cores, sample
+
+
+# -------------------------------------------------------------- our arm ----
+def run_ours(args, rank, world, local_rank, dist):
+    import paper_1601_00072_b200 as pkg
+    from paper_1601_00072_b200 import _lib
+
+    shape, c, m, eps = CONFIGS[args.config]
+    n = int(np.prod(shape))
+    max_iters = 500
+    x_full = make_volume(shape)
+
+    nccl_id = None
+    if world > 1:
+        import torch
+        buf = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            buf.copy_(torch.frombuffer(bytearray(pkg.FcmPlan.nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(buf, 0)
+        nccl_id = bytes(buf.cpu().numpy().tobytes())
+    plan = pkg.FcmPlan.for_rank(n, c, _lib.FCM_X_U8, local_rank, world, rank, nccl_id)
+    x = np.ascontiguousarray(x_full[plan.voxel0:plan.voxel0 + plan.n_local])
+    del x_full
+    plan.upload_pixels(x)
+    plan.init_membership(0)
+    plan.set_option(_lib.FCM_OPT_TIMING, 1)
+    plan.set_option(_lib.FCM_OPT_KERNEL, 0 if args.kernel == "tma" else 1)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        import torch
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        plan.run(m, eps, max_iters)
+
+    # ---- device-resident timed region: K solves, CUDA events inside fcm_run
+    barrier()
+    loop_ms, pass_ms, iters, launched = [], [], [], []
+    with ClockSampler(local_rank) as clk:
+        t_wall = time.perf_counter()
+        for _ in range(args.steps):
+            v, trace, k, conv = plan.run(m, eps, max_iters)
+            t = plan.timing()
+            loop_ms.append(t["loop_ms"])
+            pass_ms.append(t["pass_ms"])
+            iters.append(k)
+            launched.append(int(t["passes_launched"]) + 1)
+        t_wall = time.perf_counter() - t_wall
+    barrier()
+    total_ms = max_over_ranks(sum(loop_ms))
+    pass_avg = max_over_ranks(float(np.mean(pass_ms)))
+    info = plan.info()
+
+    # ---- e2e: host buffers through the C ABI (upload, solve, download)
+    u_host = np.empty(plan.n_local * c, dtype=np.float64)
+    lab_host = np.empty(plan.n_local, dtype=np.int32)
+    L = _lib.lib()
+    pinned = []
+    for arr in (x, u_host, lab_host):
+        if L.fcm_host_register(_lib.ptr(arr), arr.nbytes) == 0:
+            pinned.append(arr)
+    e2e_steps = max(1, min(args.steps, 3))
+    plan.upload_pixels(x)
+    plan.run(m, eps, max_iters)
+    plan.download(u_out=u_host, labels_out=lab_host)  # warm the download path
+    barrier()
+    t0 = time.perf_counter()
+    e2e_iters = 0
+    for _ in range(e2e_steps):
+        plan.upload_pixels(x)
+        plan.init_membership(0)
+        _, _, k, _ = plan.run(m, eps, max_iters)
+        plan.download(u_out=u_host, labels_out=lab_host)
+        e2e_iters += k
+    e2e_s = max_over_ranks(time.perf_counter() - t0)
+    for arr in pinned:
+        L.fcm_host_unregister(_lib.ptr(arr))
+
+    # sanity of what we timed (cheap, rank-local): rows sum to 1, labels valid
+    rows = u_host[: min(u_host.shape[0], 3_000_000)].reshape(-1, c).sum(axis=1)
+    assert np.abs(rows - 1.0).max() <= 1e-9
+    assert lab_host.min() >= 0 and lab_host.max() < c
+
+    if rank != 0:
+        plan.close()
+        return None
+
+    total_iters = int(sum(iters))
+    value = n * total_iters / (total_ms / 1e3)
+    peak, peak_kind = load_peaks()
+    B = algorithmic_bytes(c)
+    n_pass = plan.n_local  # voxels one pass launch of rank 0 processes
+    achieved = B * n_pass / (pass_avg / 1e3) / 1e9 if pass_avg > 0 else None
+    traffic = load_traffic(args.config)
+    out = {
+        "metric": "voxel-iterations/sec",
+        "value": value,
+        "unit": "voxel-iter/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": total_ms / args.steps,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic BrainWeb-shaped uint8 phantom (SURVEY 8(d) generator), seeded SplitMix64 start",
+        "config": {
+            "workload": f"{args.config}: {'x'.join(map(str, shape[::-1]))} volume, c={c}, m={m}, eps={eps}",
+            "n_voxels": n, "c": c, "m": m, "epsilon": eps, "seed": 0,
+            "iterations_per_solve": iters[0],
+            "step": "one fcm_run: device seeded start + fused passes to convergence",
+            "l2": "inputs larger than L2 (x u8 + two fp32 SoA membership planes per iteration)",
+            "parallelism": f"voxel shards x{world}, ncclAllGather of 2c+2 roots per iteration"
+            if world > 1 else "1 GPU",
+        },
+        "hbm_gbs_per_gpu": B * n / world * total_iters / (total_ms / 1e3) / 1e9,
+        "pass_ms": pass_avg,
+        "roofline": {
+            "bound": "hbm",
+            "achieved": achieved,
+            "peak": peak,
+            "unit": "GB/s",
+            "frac": (achieved / peak) if achieved else None,
+            "traffic": traffic,
+            "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured" else peak_kind,
+            "bytes_per_voxel_iter": B,
+            "kernel": ("pass_tma_kernel" if args.kernel == "tma" else "pass_kernel")
+            + ("<uint8_t,%d,MODE_M2>" % c if m == 2.0 else "<uint8_t,%d,MODE_GEN>" % c),
+        },
+        "e2e": {
+            "value": n * e2e_iters / e2e_s,
+            "unit": "voxel-iter/s",
+            "h2d_bytes_per_step": int(x.nbytes),
+            "d2h_bytes_per_step": int(u_host.nbytes + lab_host.nbytes),
+        },
+        "gpu_launches": int(sum(launched)),
+        "clocks": clk.summary(),
+        "plan": {k: info[k] for k in ("tile", "tiles", "tiles_local", "grid", "dev_bytes")},
+        "wall_s_timed": t_wall,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        v, kind, cores, sample = cpu_reference_sample(shape, c, m, eps)
+        out["cpu_baseline"] = {"value": v, "unit": "voxel-iter/s", "cores": cores, "kind": kind, "sample": sample}
+    plan.close()
+    return out
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return None
+    shape, c, m, eps = CONFIGS[args.config]
+    vals = []
+    kind = cores = sample = None
+    for _ in range(args.warmup):
+        cpu_reference_sample(shape, c, m, eps, slab=8, iters=1)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        v, kind, cores, sample = cpu_reference_sample(shape, c, m, eps, slab=16, iters=2)
+        vals.append(v)
+    dt = time.perf_counter() - t0
+    value = float(np.mean(vals))
+    return {
+        "metric": "voxel-iterations/sec",
+        "value": value,
+        "unit": "voxel-iter/s",
+        "impl": "reference",
+        "n_gpus": 0,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": dt / args.steps * 1e3,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic BrainWeb-shaped uint8 phantom slab (host float64), seeded SplitMix64 start",
+        "config": {"workload": f"{args.config}: {'x'.join(map(str, shape[::-1]))} volume, c={c}, m={m}, eps={eps}",
+                   "n_voxels": int(np.prod(shape)), "c": c, "m": m, "epsilon": eps},
+        "cpu_baseline": {"value": value, "unit": "voxel-iter/s", "cores": cores, "kind": kind, "sample": sample},
+        "e2e": {"value": value, "unit": "voxel-iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C4", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--kernel", default="tma", choices=["tma", "ldg"],
+                    help="pass kernel: TMA bulk-copy pipeline (default) or register-staged LDG/STG")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if args.impl == "reference":
+        out = run_reference(args, rank)
+    else:
+        if world > 1:
+            import torch
+            import torch.distributed as dist
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("nccl")
+        out = run_ours(args, rank, world, local_rank, dist)
+        if dist is not None:
+            dist.barrier()
+            dist.destroy_process_group()
+    if out is not None:
+        print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,153 @@
+/*
+ * fcm_b200.h -- C ABI of the B200 Fuzzy C-Means hot path (libfcm_b200.so).
+ *
+ * Drop-in boundary for the reference package fcmseg (/root/reference/pkg).
+ * The reference has no FFI of its own: its hot path is the Python engine loop
+ * core._iterate / parallel._iterate calling a kernel module chosen by
+ * backend.active() (backend.py:11-52).  Two cuts are exported:
+ *
+ *   1. the ENGINE-LOOP boundary (the one the product uses): a plan holding
+ *      device-resident pixels and memberships runs the whole
+ *      centers -> membership -> delta -> objective loop on the GPU and
+ *      returns what _iterate returns (v, u, iterations, trace, converged).
+ *      Replaces core._iterate (core.py:105-132), parallel._iterate
+ *      (parallel.py:257-331), core.init_membership (core.py:24-39) and
+ *      core.defuzzify (core.py:94-102).
+ *   2. the KERNEL seam: the functions of _kernels.pyx (:33-238) that have a
+ *      meaning on their own, on caller-owned host buffers with the
+ *      reference's conventions (flat float64, membership AoS u[i*c + j],
+ *      int32 labels, -1 / cluster-index return for a dead cluster).
+ *
+ * All functions return an fcm_status.  Host buffers stay caller-owned; the
+ * plan owns every device buffer.  A plan is not re-entrant: use one plan per
+ * host thread.  There is no CPU fallback: without a usable sm_100 GPU every
+ * entry point that computes returns FCM_E_CUDA.
+ */
+#ifndef FCM_B200_H
+#define FCM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FCM_ABI_VERSION 1
+
+typedef enum {
+  FCM_OK = 0,
+  FCM_E_ARG = 1,        /* invalid argument            -> InvalidConfigError / DimensionMismatchError */
+  FCM_E_CUDA = 2,       /* CUDA runtime failure / no GPU */
+  FCM_E_NCCL = 3,       /* NCCL failure (multi-process plans) */
+  FCM_E_DEGENERATE = 4, /* a cluster got zero weight   -> DegenerateClusterError(dead_cluster), core.py:121-123 */
+  FCM_E_STATE = 5,      /* call order violated (e.g. run before upload) */
+  FCM_E_NOMEM = 6       /* device allocation failed */
+} fcm_status;
+
+typedef enum {
+  FCM_X_U8 = 0,  /* integer intensities 0..255 (every BASELINE config): 1 byte per voxel in HBM */
+  FCM_X_F64 = 2  /* any finite, non-negative intensity (types.py:38-41) */
+} fcm_x_kind;
+
+typedef enum {
+  FCM_OPT_BATCH = 1,   /* passes launched between host checks of the done flag (default 8) */
+  FCM_OPT_TIMING = 2,  /* 1: record per-pass CUDA events for fcm_last_timing (default 0) */
+  FCM_OPT_GRID = 3,    /* force CTAs per pass launch (0 = occupancy-derived, default) */
+  FCM_OPT_KERNEL = 4   /* pass kernel: 0 = TMA bulk-copy pipeline (default), 1 = register-staged LDG/STG */
+} fcm_option;
+
+typedef struct fcm_plan fcm_plan;
+
+int fcm_abi_version(void);
+const char* fcm_status_string(int status);
+int fcm_device_count(int32_t* count);
+
+/* ------------------------------------------------------------------------
+ * Engine loop (replaces core._iterate / parallel._iterate)
+ * ---------------------------------------------------------------------- */
+
+/* Single-process plan over n voxels and c clusters (2 <= c <= 16), sharded
+ * over nshards in {1,2,4,8} shards placed on devices[0..nshards-1] (a device
+ * may repeat: shards on one GPU exercise the multi-GPU reduction exactly).
+ * Mirrors run_fcm_parallel's workers= (parallel.py:334-362): results are
+ * bit-identical for every shard count. */
+int fcm_plan_create(fcm_plan** out, int64_t n, int32_t c, int32_t x_kind, int32_t nshards,
+                    const int32_t* devices);
+
+/* One rank of an nranks-process job (one process per GPU): the plan owns the
+ * rank's contiguous voxel range (query it with fcm_plan_info) and exchanges
+ * the 2c+2 reduction roots with ncclAllGather.  nccl_id is the 128-byte
+ * ncclUniqueId from fcm_nccl_unique_id on rank 0 (ignored when nranks == 1). */
+int fcm_plan_create_rank(fcm_plan** out, int64_t n_global, int32_t c, int32_t x_kind,
+                         int32_t device, int32_t nranks, int32_t rank, const void* nccl_id);
+int fcm_nccl_unique_id(void* out128);
+
+/* Host-only: the voxel range and reduction-tree geometry of `rank` in an
+ * nranks job over n voxels (no GPU needed).  out[0..]: n_local, voxel0,
+ * tile voxels, tiles T, tiles per octant M, groups per octant, first octant,
+ * octants, first tile, tiles_local. */
+int fcm_geometry(int64_t n, int32_t nranks, int32_t rank, int64_t* out, int32_t count);
+
+int fcm_plan_destroy(fcm_plan* plan);
+const char* fcm_last_error(const fcm_plan* plan);
+int fcm_set_option(fcm_plan* plan, int32_t key, int64_t value);
+
+/* info[0..]: n_global, n_local (voxels of the plan's range: the whole image
+ * for fcm_plan_create, the rank's slice for fcm_plan_create_rank), voxel0
+ * (first voxel of that range), tile voxels, tiles (global), tiles of the
+ * plan, grid of the last pass, nshards, bytes of device memory held. */
+int fcm_plan_info(const fcm_plan* plan, int64_t* info, int32_t count);
+
+/* Pixels of the plan's voxel range (whole image for fcm_plan_create, the
+ * rank's [voxel0, voxel0 + n_local) slice for fcm_plan_create_rank), in the
+ * plan's x_kind (uint8_t or double). */
+int fcm_upload_pixels(fcm_plan* plan, const void* x);
+
+/* Initial membership, exactly one of:
+ *   fcm_init_membership  -- seeded SplitMix64 rows generated on the device,
+ *                           bit-identical to core.init_membership
+ *                           (_kernels.pyx:44-69); nothing crosses PCIe.
+ *   fcm_upload_membership-- caller-provided AoS float64 rows of the plan's
+ *                           voxel range (initial_membership=, core.py:135-143). */
+int fcm_init_membership(fcm_plan* plan, uint64_t seed);
+int fcm_upload_membership(fcm_plan* plan, const double* u0_aos);
+
+/* Run the loop to convergence (delta < epsilon) or max_iters passes.
+ * v_out[c] receives the centers that produced the final membership
+ * (core.py:132), trace_out[max_iters] the objective per iteration.
+ * Returns FCM_E_DEGENERATE with *dead_cluster set when a cluster weight sum
+ * is exactly zero.  Each fcm_run restarts from the initial membership. */
+int fcm_run(fcm_plan* plan, double m, double epsilon, int32_t max_iters, double* v_out,
+            double* trace_out, int32_t* iterations, int32_t* converged, int32_t* dead_cluster);
+
+/* Final membership (AoS float64, rows sum to 1 within 1e-9; types.py:82-85)
+ * and defuzzified labels (argmax, ties -> lowest index; _kernels.pyx:223-238)
+ * of the plan's voxel range.  Either pointer may be NULL. */
+int fcm_download(fcm_plan* plan, double* u_aos_out, int32_t* labels_out);
+
+/* out[0..]: ms of the last fcm_run's device loop (prologue + passes, CUDA
+ * events), mean ms per pass (when FCM_OPT_TIMING), prologue ms, passes
+ * launched, passes that did work. */
+int fcm_last_timing(const fcm_plan* plan, double* out, int32_t count);
+
+/* Page-lock caller memory so uploads/downloads run at full PCIe speed. */
+int fcm_host_register(void* ptr, int64_t bytes);
+int fcm_host_unregister(void* ptr);
+
+/* ------------------------------------------------------------------------
+ * Kernel seam (_kernels.pyx), host buffers, one call = one GPU op
+ * ---------------------------------------------------------------------- */
+int fcm_fill_membership_random(double* u_out, int64_t n, int32_t c, uint64_t seed, int32_t device);
+int fcm_update_centers(const double* x, const double* u, double* v_out, int64_t n, int32_t c,
+                       double m, int32_t device, int32_t* dead_out);
+int fcm_update_membership(const double* x, const double* v, double* u_out, int64_t n, int32_t c,
+                          double m, int32_t device);
+int fcm_objective(const double* x, const double* u, const double* v, int64_t n, int32_t c,
+                  double m, int32_t device, double* out);
+int fcm_max_abs_diff(const double* a, const double* b, int64_t count, int32_t device, double* out);
+int fcm_argmax_rows(const double* u, int32_t* labels_out, int64_t n, int32_t c, int32_t device);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FCM_B200_H */

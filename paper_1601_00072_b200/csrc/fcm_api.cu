@@ -1,0 +1,951 @@
+// fcm_api.cu -- host runtime behind include/fcm_b200.h.
+//
+// A plan owns, per shard: the pixels (uint8 or fp64, padded to whole tiles),
+// two fp32 SoA membership buffers (u_{k-1}, u_k), the reduction tree scratch
+// and a Control block.  fcm_run enqueues prologue + passes in batches on the
+// shard streams and only syncs once per batch to read the device `done` flag
+// (core._iterate's Python loop, core.py:105-132, becomes a device loop).
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include <nccl.h>
+
+#include "../../include/fcm_b200.h"
+#include "fcm_kernels.h"
+#include "fcm_ops.h"
+
+using namespace fcm;
+
+// ------------------------------------------------------------------ NCCL ---
+// Loaded on first use so the library (and single-GPU plans) do not depend on
+// libnccl being present.
+namespace {
+struct NcclApi {
+  bool tried = false, ok = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+NcclApi g_nccl;
+
+bool load_nccl() {
+  if (g_nccl.tried) return g_nccl.ok;
+  g_nccl.tried = true;
+  const char* names[] = {"libnccl.so.2", "libnccl.so", nullptr};
+  void* h = nullptr;
+  const char* env = getenv("FCM_NCCL_LIB");
+  if (env) h = dlopen(env, RTLD_NOW | RTLD_GLOBAL);
+  for (int i = 0; !h && names[i]; ++i) h = dlopen(names[i], RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return false;
+  g_nccl.GetUniqueId = (decltype(g_nccl.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+  g_nccl.CommInitRank = (decltype(g_nccl.CommInitRank))dlsym(h, "ncclCommInitRank");
+  g_nccl.AllGather = (decltype(g_nccl.AllGather))dlsym(h, "ncclAllGather");
+  g_nccl.CommDestroy = (decltype(g_nccl.CommDestroy))dlsym(h, "ncclCommDestroy");
+  g_nccl.GetErrorString = (decltype(g_nccl.GetErrorString))dlsym(h, "ncclGetErrorString");
+  g_nccl.ok = g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.AllGather && g_nccl.CommDestroy;
+  return g_nccl.ok;
+}
+}  // namespace
+
+// ------------------------------------------------------------------ plan ---
+namespace {
+struct Shard {
+  int device = 0;
+  int sms = 148;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev_pass = nullptr;
+  Geometry g{};
+  void* x = nullptr;
+  float* u[2] = {nullptr, nullptr};
+  double* u0_aos = nullptr;
+  double* tile_part = nullptr;
+  double* group_root = nullptr;
+  double* oct_root = nullptr;
+  double* rank_root = nullptr;  // [2][nf], double-buffered by pass parity
+  double* gathered = nullptr;   // [nranks][nf] (NCCL)
+  unsigned* group_cnt = nullptr;
+  unsigned* oct_cnt = nullptr;
+  Control* ctl = nullptr;
+  double* trace = nullptr;
+  int trace_cap = 0;
+  double* out_u = nullptr;
+  int32_t* out_labels = nullptr;
+  int last_grid = 0;
+  std::vector<void*> allocs;
+};
+}  // namespace
+
+struct fcm_plan {
+  int64_t n_global = 0;
+  int c = 0;
+  int xkind = XK_U8;
+  int nshards = 1;     // shards driven by this process
+  int nranks = 1;      // ranks of the whole job (== nshards for single-process plans)
+  int rank = 0;        // rank of shard 0 (NCCL plans)
+  bool use_nccl = false;
+  ncclComm_t comm = nullptr;
+  Shard sh[kOctants];
+  int init_src = 0;  // 0 none, 1 seed, 2 uploaded AoS
+  uint64_t seed = 0;
+  bool x_ready = false;
+  bool run_ok = false;
+  int mode = MODE_M2;
+  Powers pw{};
+  int batch = 8;
+  int timing = 0;
+  int force_grid = 0;
+  int variant = 0;  // pass kernel: 0 TMA pipeline, 1 register-staged LDG
+  Control* host_ctl = nullptr;   // pinned: device -> host reads of the control block
+  Control* host_tmpl = nullptr;  // pinned: reset template copied to every shard
+  std::vector<cudaEvent_t> ev_t0, ev_t1;
+  cudaEvent_t ev_start = nullptr, ev_pro = nullptr, ev_end = nullptr;
+  double t_loop_ms = 0, t_pass_ms = 0, t_pro_ms = 0;
+  int passes_launched = 0, passes_done = 0;
+  int64_t dev_bytes = 0;
+  std::string err;
+};
+
+namespace {
+int fail(fcm_plan* p, int code, const char* fmt, ...) {
+  if (p) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    p->err = buf;
+  }
+  return code;
+}
+
+#define CK(expr)                                                                              \
+  do {                                                                                        \
+    cudaError_t e_ = (expr);                                                                  \
+    if (e_ != cudaSuccess)                                                                    \
+      return fail(p, FCM_E_CUDA, "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(e_),      \
+                  __FILE__, __LINE__);                                                        \
+  } while (0)
+
+int nf_of(int c) { return 2 * c + 2; }
+
+int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Global tile tree ("Deterministic reduction").  Depends only on n.
+void base_geometry(int64_t n, Geometry& g) {
+  int64_t tile = 1024;
+  while (tile < ceil_div(n, 8192)) tile <<= 1;
+  while (tile < 4096 && n / tile > 2048) tile <<= 1;
+  int shift = 0;
+  while ((int64_t(1) << shift) < tile) ++shift;
+  g.n_global = n;
+  g.tile_shift = shift;
+  g.T = (int)ceil_div(n, tile);
+  const int T8 = (int)ceil_div(g.T, kOctants) * kOctants;
+  g.M = T8 / kOctants;
+  g.gpo = (int)ceil_div(g.M, kGroup);
+}
+
+void rank_geometry(Geometry& g, int nranks, int rank) {
+  const int64_t tile = int64_t(1) << g.tile_shift;
+  g.nranks = nranks;
+  g.rank = rank;
+  g.noct = kOctants / nranks;
+  g.oct0 = rank * g.noct;
+  g.tile0 = g.oct0 * g.M;
+  const int tend = std::min((g.oct0 + g.noct) * g.M, g.T);
+  g.tiles_local = std::max(0, tend - g.tile0);
+  g.voxel0 = (int64_t)g.tile0 * tile;
+  const int64_t vend = std::min((int64_t)tend * tile, g.n_global);
+  g.n_local = std::max<int64_t>(0, vend - g.voxel0);
+  if (g.tiles_local == 0) g.voxel0 = std::min(g.voxel0, g.n_global);
+  g.plane = (int64_t)std::max(g.tiles_local, 1) * tile;
+}
+
+template <typename T>
+int dalloc(fcm_plan* p, Shard& s, T** ptr, size_t count) {
+  void* q = nullptr;
+  size_t bytes = std::max<size_t>(count, 1) * sizeof(T);
+  cudaError_t e = cudaMalloc(&q, bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(p, FCM_E_NOMEM, "cudaMalloc(%zu bytes) on device %d failed: %s", bytes, s.device,
+                cudaGetErrorString(e));
+  }
+  s.allocs.push_back(q);
+  p->dev_bytes += (int64_t)bytes;
+  *ptr = (T*)q;
+  return FCM_OK;
+}
+
+int setup_shard(fcm_plan* p, Shard& s) {
+  CK(cudaSetDevice(s.device));
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, s.device));
+  if (prop.major < 10)
+    return fail(p, FCM_E_CUDA, "device %d is sm_%d%d; this build targets sm_100a", s.device,
+                prop.major, prop.minor);
+  s.sms = prop.multiProcessorCount;
+  CK(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&s.ev_pass, cudaEventDisableTiming));
+  const int nf = nf_of(p->c);
+  const size_t xsz = p->xkind == XK_U8 ? 1 : 8;
+  int rc;
+  uint8_t* xb = nullptr;
+  if ((rc = dalloc(p, s, &xb, s.g.plane * xsz))) return rc;
+  s.x = xb;
+  CK(cudaMemsetAsync(s.x, 0, s.g.plane * xsz, s.stream));
+  for (int b = 0; b < 2; ++b)
+    if ((rc = dalloc(p, s, &s.u[b], (size_t)s.g.plane * p->c))) return rc;
+  if ((rc = dalloc(p, s, &s.tile_part, (size_t)std::max(s.g.tiles_local, 1) * nf))) return rc;
+  if ((rc = dalloc(p, s, &s.group_root, (size_t)s.g.noct * s.g.gpo * nf))) return rc;
+  if ((rc = dalloc(p, s, &s.oct_root, (size_t)s.g.noct * nf))) return rc;
+  if ((rc = dalloc(p, s, &s.rank_root, (size_t)2 * nf))) return rc;
+  if ((rc = dalloc(p, s, &s.gathered, (size_t)p->nranks * nf))) return rc;
+  if ((rc = dalloc(p, s, &s.group_cnt, (size_t)s.g.noct * s.g.gpo))) return rc;
+  if ((rc = dalloc(p, s, &s.oct_cnt, (size_t)s.g.noct))) return rc;
+  if ((rc = dalloc(p, s, &s.ctl, 1))) return rc;
+  CK(cudaMemsetAsync(s.group_cnt, 0, sizeof(unsigned) * s.g.noct * s.g.gpo, s.stream));
+  CK(cudaMemsetAsync(s.oct_cnt, 0, sizeof(unsigned) * s.g.noct, s.stream));
+  CK(cudaMemsetAsync(s.ctl, 0, sizeof(Control), s.stream));
+  return FCM_OK;
+}
+
+void release(fcm_plan* p) {
+  for (int i = 0; i < p->nshards; ++i) {
+    Shard& s = p->sh[i];
+    cudaSetDevice(s.device);
+    if (s.stream) cudaStreamSynchronize(s.stream);
+    for (void* q : s.allocs) cudaFree(q);
+    s.allocs.clear();
+    if (s.ev_pass) cudaEventDestroy(s.ev_pass);
+    if (s.stream) cudaStreamDestroy(s.stream);
+  }
+  if (p->nshards > 0) cudaSetDevice(p->sh[0].device);
+  for (auto e : p->ev_t0) cudaEventDestroy(e);
+  for (auto e : p->ev_t1) cudaEventDestroy(e);
+  if (p->ev_start) cudaEventDestroy(p->ev_start);
+  if (p->ev_pro) cudaEventDestroy(p->ev_pro);
+  if (p->ev_end) cudaEventDestroy(p->ev_end);
+  if (p->host_ctl) cudaFreeHost(p->host_ctl);
+  if (p->host_tmpl) cudaFreeHost(p->host_tmpl);
+  if (p->comm && g_nccl.ok) g_nccl.CommDestroy(p->comm);
+}
+
+int common_setup(fcm_plan* p) {
+  int rc;
+  for (int i = 0; i < p->nshards; ++i)
+    if ((rc = setup_shard(p, p->sh[i]))) return rc;
+  // Peer access for single-process multi-device plans: each finalize reads
+  // every shard's 2c+2-double root directly over NVLink.
+  for (int i = 0; i < p->nshards; ++i)
+    for (int j = 0; j < p->nshards; ++j) {
+      const int di = p->sh[i].device, dj = p->sh[j].device;
+      if (di == dj) continue;
+      int can = 0;
+      CK(cudaDeviceCanAccessPeer(&can, di, dj));
+      if (!can) return fail(p, FCM_E_CUDA, "device %d cannot access peer %d", di, dj);
+      CK(cudaSetDevice(di));
+      cudaError_t e = cudaDeviceEnablePeerAccess(dj, 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) CK(e);
+      cudaGetLastError();
+    }
+  CK(cudaSetDevice(p->sh[0].device));
+  CK(cudaMallocHost(&p->host_ctl, sizeof(Control)));
+  CK(cudaMallocHost(&p->host_tmpl, sizeof(Control)));
+  CK(cudaEventCreate(&p->ev_start));
+  CK(cudaEventCreate(&p->ev_pro));
+  CK(cudaEventCreate(&p->ev_end));
+  for (int i = 0; i < p->nshards; ++i) {
+    CK(cudaSetDevice(p->sh[i].device));
+    CK(cudaStreamSynchronize(p->sh[i].stream));
+  }
+  return FCM_OK;
+}
+
+void set_powers(fcm_plan* p, double m) {
+  Powers& w = p->pw;
+  w.m = m;
+  w.p = 2.0 / (m - 1.0);  // _kernels.pyx:96
+  const double pr = std::nearbyint(w.p);
+  if (w.p == pr && pr >= 1.0 && pr <= 64.0) {
+    w.pkind = PK_INT;
+    w.pint = (int)pr;
+  } else {
+    w.pkind = PK_REAL;
+    w.pint = 0;
+  }
+  const double mr = std::nearbyint(m), m2 = std::nearbyint(2.0 * m);
+  if (m == mr && m <= 64.0) {
+    w.mkind = MK_INT;
+    w.mint = (int)mr;
+  } else if (2.0 * m == m2 && m <= 64.0) {
+    w.mkind = MK_HALF;
+    w.mint = (int)std::floor(m);
+  } else {
+    w.mkind = MK_REAL;
+    w.mint = 0;
+  }
+  p->mode = (m == 2.0) ? MODE_M2 : MODE_GEN;
+}
+
+PassArgs make_args(fcm_plan* p, Shard& s, int seq, double eps, int max_iters) {
+  PassArgs a{};
+  const int nf = nf_of(p->c);
+  a.x = s.x;
+  a.u_cur = s.u[(seq + 1) & 1];  // pass seq reads u[(seq-1)&1]
+  a.u_nxt = s.u[seq & 1];        // prologue (seq 0) writes u[0]
+  a.u0_aos = s.u0_aos;
+  a.seed = p->seed;
+  a.c = p->c;
+  a.m = p->pw.m;
+  a.p = p->pw.p;
+  a.pkind = p->pw.pkind;
+  a.pint = p->pw.pint;
+  a.mkind = p->pw.mkind;
+  a.mint = p->pw.mint;
+  a.eps = eps;
+  a.max_iters = max_iters;
+  a.seq = seq;
+  a.g = s.g;
+  a.tile_part = s.tile_part;
+  a.group_root = s.group_root;
+  a.oct_root = s.oct_root;
+  a.rank_root = s.rank_root + (seq & 1) * nf;
+  a.group_cnt = s.group_cnt;
+  a.oct_cnt = s.oct_cnt;
+  a.ctl = s.ctl;
+  a.trace = s.trace;
+  return a;
+}
+
+// Launch one prologue (seq == 0) or pass on every shard, then -- when the
+// job has more than one rank -- exchange the roots and finalize everywhere.
+int step(fcm_plan* p, int seq, double eps, int max_iters) {
+  const int nf = nf_of(p->c);
+  const bool prologue = seq == 0;
+  for (int i = 0; i < p->nshards; ++i) {
+    Shard& s = p->sh[i];
+    CK(cudaSetDevice(s.device));
+    const PassArgs a = make_args(p, s, seq, eps, max_iters);
+    if (s.g.tiles_local == 0) {
+      CK(cudaMemsetAsync(a.rank_root, 0, sizeof(double) * nf, s.stream));
+    } else if (prologue) {
+      CK(launch_prologue(p->xkind, p->c, p->init_src == 1, a, s.sms, s.stream));
+    } else {
+      int grid = 0;
+      const bool t = p->timing && i == 0;
+      if (t) {
+        size_t k = (size_t)p->passes_launched;
+        while (p->ev_t0.size() <= k) {
+          cudaEvent_t e0, e1;
+          CK(cudaEventCreate(&e0));
+          CK(cudaEventCreate(&e1));
+          p->ev_t0.push_back(e0);
+          p->ev_t1.push_back(e1);
+        }
+        CK(cudaEventRecord(p->ev_t0[k], s.stream));
+      }
+      PassArgs b = a;
+      CK(launch_pass(p->xkind, p->c, p->mode, b, s.sms, s.stream, &grid, p->variant, p->force_grid));
+      if (t) CK(cudaEventRecord(p->ev_t1[(size_t)p->passes_launched], s.stream));
+      s.last_grid = grid;
+    }
+  }
+  if (!prologue) p->passes_launched++;
+  if (p->nranks == 1) return FCM_OK;
+
+  FinalizeArgs f{};
+  f.nranks = p->nranks;
+  f.c = p->c;
+  f.eps = eps;
+  f.max_iters = max_iters;
+  f.prologue = prologue ? 1 : 0;
+  if (p->use_nccl) {
+    Shard& s = p->sh[0];
+    ncclResult_t r = g_nccl.AllGather(s.rank_root + (seq & 1) * nf, s.gathered, (size_t)nf,
+                                      ncclDouble, p->comm, s.stream);
+    if (r != ncclSuccess)
+      return fail(p, FCM_E_NCCL, "ncclAllGather: %s", g_nccl.GetErrorString(r));
+    for (int r2 = 0; r2 < p->nranks; ++r2) f.roots[r2] = s.gathered + r2 * nf;
+    f.ctl = s.ctl;
+    f.trace = s.trace;
+    CK(launch_finalize(f, s.stream));
+    return FCM_OK;
+  }
+  for (int i = 0; i < p->nshards; ++i) {
+    CK(cudaSetDevice(p->sh[i].device));
+    CK(cudaEventRecord(p->sh[i].ev_pass, p->sh[i].stream));
+  }
+  for (int r2 = 0; r2 < p->nshards; ++r2) f.roots[r2] = p->sh[r2].rank_root + (seq & 1) * nf;
+  for (int i = 0; i < p->nshards; ++i) {
+    Shard& s = p->sh[i];
+    CK(cudaSetDevice(s.device));
+    for (int j = 0; j < p->nshards; ++j)
+      if (j != i) CK(cudaStreamWaitEvent(s.stream, p->sh[j].ev_pass, 0));
+    f.ctl = s.ctl;
+    f.trace = s.trace;
+    CK(launch_finalize(f, s.stream));
+  }
+  return FCM_OK;
+}
+
+int check_plan(fcm_plan* p) { return p ? FCM_OK : FCM_E_ARG; }
+}  // namespace
+
+// ================================================================== C ABI ==
+extern "C" {
+
+int fcm_abi_version(void) { return FCM_ABI_VERSION; }
+
+const char* fcm_status_string(int status) {
+  switch (status) {
+    case FCM_OK: return "ok";
+    case FCM_E_ARG: return "invalid argument";
+    case FCM_E_CUDA: return "CUDA error";
+    case FCM_E_NCCL: return "NCCL error";
+    case FCM_E_DEGENERATE: return "degenerate cluster";
+    case FCM_E_STATE: return "invalid call order";
+    case FCM_E_NOMEM: return "out of device memory";
+    default: return "unknown status";
+  }
+}
+
+int fcm_device_count(int32_t* count) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    if (count) *count = 0;
+    return FCM_E_CUDA;
+  }
+  if (count) *count = n;
+  return FCM_OK;
+}
+
+static int validate_create(int64_t n, int32_t c, int32_t x_kind) {
+  if (n < 1 || c < 2 || c > kCMaxSupported || n < c) return FCM_E_ARG;
+  if (x_kind != FCM_X_U8 && x_kind != FCM_X_F64) return FCM_E_ARG;
+  if (n > (int64_t)8192 * (int64_t(1) << 30)) return FCM_E_ARG;
+  return FCM_OK;
+}
+
+int fcm_plan_create(fcm_plan** out, int64_t n, int32_t c, int32_t x_kind, int32_t nshards,
+                    const int32_t* devices) {
+  if (!out) return FCM_E_ARG;
+  *out = nullptr;
+  if (validate_create(n, c, x_kind)) return FCM_E_ARG;
+  if (nshards != 1 && nshards != 2 && nshards != 4 && nshards != 8) return FCM_E_ARG;
+  fcm_plan* p = new fcm_plan();
+  p->n_global = n;
+  p->c = c;
+  p->xkind = x_kind == FCM_X_U8 ? XK_U8 : XK_F64;
+  p->nshards = nshards;
+  p->nranks = nshards;
+  Geometry base{};
+  base_geometry(n, base);
+  for (int i = 0; i < nshards; ++i) {
+    p->sh[i].device = devices ? devices[i] : 0;
+    p->sh[i].g = base;
+    rank_geometry(p->sh[i].g, nshards, i);
+  }
+  int rc = common_setup(p);
+  if (rc) {
+    fprintf(stderr, "fcm_plan_create: %s\n", p->err.c_str());
+    release(p);
+    delete p;
+    return rc;
+  }
+  *out = p;
+  return FCM_OK;
+}
+
+int fcm_geometry(int64_t n, int32_t nranks, int32_t rank, int64_t* out, int32_t count) {
+  if (!out || n < 1 || (nranks != 1 && nranks != 2 && nranks != 4 && nranks != 8) || rank < 0 ||
+      rank >= nranks)
+    return FCM_E_ARG;
+  Geometry g{};
+  base_geometry(n, g);
+  rank_geometry(g, nranks, rank);
+  const int64_t v[] = {g.n_local, g.voxel0, int64_t(1) << g.tile_shift, g.T, g.M,
+                       g.gpo, g.oct0, g.noct, g.tile0, g.tiles_local};
+  for (int i = 0; i < count && i < (int)(sizeof v / sizeof v[0]); ++i) out[i] = v[i];
+  return FCM_OK;
+}
+
+int fcm_nccl_unique_id(void* out128) {
+  if (!out128) return FCM_E_ARG;
+  if (!load_nccl()) return FCM_E_NCCL;
+  ncclUniqueId id;
+  if (g_nccl.GetUniqueId(&id) != ncclSuccess) return FCM_E_NCCL;
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+  memcpy(out128, &id, sizeof id);
+  return FCM_OK;
+}
+
+int fcm_plan_create_rank(fcm_plan** out, int64_t n_global, int32_t c, int32_t x_kind,
+                         int32_t device, int32_t nranks, int32_t rank, const void* nccl_id) {
+  if (!out) return FCM_E_ARG;
+  *out = nullptr;
+  if (validate_create(n_global, c, x_kind)) return FCM_E_ARG;
+  if (nranks != 1 && nranks != 2 && nranks != 4 && nranks != 8) return FCM_E_ARG;
+  if (rank < 0 || rank >= nranks) return FCM_E_ARG;
+  fcm_plan* p = new fcm_plan();
+  p->n_global = n_global;
+  p->c = c;
+  p->xkind = x_kind == FCM_X_U8 ? XK_U8 : XK_F64;
+  p->nshards = 1;
+  p->nranks = nranks;
+  p->rank = rank;
+  p->sh[0].device = device;
+  base_geometry(n_global, p->sh[0].g);
+  rank_geometry(p->sh[0].g, nranks, rank);
+  int rc = common_setup(p);
+  if (!rc && nranks > 1) {
+    if (!nccl_id || !load_nccl()) {
+      rc = fail(p, FCM_E_NCCL, "NCCL unavailable (set FCM_NCCL_LIB) or no unique id");
+    } else {
+      ncclUniqueId id;
+      memcpy(&id, nccl_id, sizeof id);
+      cudaSetDevice(device);
+      ncclResult_t r = g_nccl.CommInitRank(&p->comm, nranks, id, rank);
+      if (r != ncclSuccess) rc = fail(p, FCM_E_NCCL, "ncclCommInitRank: %s", g_nccl.GetErrorString(r));
+      else p->use_nccl = true;
+    }
+  }
+  if (rc) {
+    fprintf(stderr, "fcm_plan_create_rank: %s\n", p->err.c_str());
+    release(p);
+    delete p;
+    return rc;
+  }
+  *out = p;
+  return FCM_OK;
+}
+
+int fcm_plan_destroy(fcm_plan* p) {
+  if (!p) return FCM_OK;
+  release(p);
+  delete p;
+  return FCM_OK;
+}
+
+const char* fcm_last_error(const fcm_plan* p) { return p ? p->err.c_str() : "null plan"; }
+
+int fcm_set_option(fcm_plan* p, int32_t key, int64_t value) {
+  if (check_plan(p)) return FCM_E_ARG;
+  switch (key) {
+    case FCM_OPT_BATCH:
+      if (value < 1 || value > 4096) return FCM_E_ARG;
+      p->batch = (int)value;
+      return FCM_OK;
+    case FCM_OPT_TIMING: p->timing = value ? 1 : 0; return FCM_OK;
+    case FCM_OPT_GRID:
+      if (value < 0) return FCM_E_ARG;
+      p->force_grid = (int)value;
+      return FCM_OK;
+    case FCM_OPT_KERNEL:
+      if (value != 0 && value != 1) return FCM_E_ARG;
+      p->variant = (int)value;
+      return FCM_OK;
+    default: return FCM_E_ARG;
+  }
+}
+
+int fcm_plan_info(const fcm_plan* p, int64_t* info, int32_t count) {
+  if (!p || !info) return FCM_E_ARG;
+  // The plan's voxel range: the whole image for single-process plans, the
+  // rank's slice for NCCL rank plans.
+  const Geometry& g = p->sh[0].g;
+  int64_t n_plan = 0, tiles_plan = 0;
+  for (int i = 0; i < p->nshards; ++i) {
+    n_plan += p->sh[i].g.n_local;
+    tiles_plan += p->sh[i].g.tiles_local;
+  }
+  const int64_t v[] = {p->n_global, n_plan, g.voxel0, int64_t(1) << g.tile_shift, g.T,
+                       tiles_plan, p->sh[0].last_grid, p->nshards, p->dev_bytes};
+  for (int i = 0; i < count && i < (int)(sizeof v / sizeof v[0]); ++i) info[i] = v[i];
+  return FCM_OK;
+}
+
+int fcm_upload_pixels(fcm_plan* p, const void* x) {
+  if (check_plan(p) || !x) return FCM_E_ARG;
+  const size_t xsz = p->xkind == XK_U8 ? 1 : 8;
+  const int64_t host0 = p->use_nccl ? p->sh[0].g.voxel0 : 0;
+  for (int i = 0; i < p->nshards; ++i) {
+    Shard& s = p->sh[i];
+    if (s.g.n_local == 0) continue;
+    CK(cudaSetDevice(s.device));
+    const char* src = (const char*)x + (s.g.voxel0 - host0) * xsz;
+    CK(cudaMemcpyAsync(s.x, src, s.g.n_local * xsz, cudaMemcpyHostToDevice, s.stream));
+  }
+  for (int i = 0; i < p->nshards; ++i) {
+    CK(cudaSetDevice(p->sh[i].device));
+    CK(cudaStreamSynchronize(p->sh[i].stream));
+  }
+  p->x_ready = true;
+  return FCM_OK;
+}
+
+int fcm_init_membership(fcm_plan* p, uint64_t seed) {
+  if (check_plan(p)) return FCM_E_ARG;
+  p->init_src = 1;
+  p->seed = seed;
+  return FCM_OK;
+}
+
+int fcm_upload_membership(fcm_plan* p, const double* u0) {
+  if (check_plan(p) || !u0) return FCM_E_ARG;
+  const int64_t host0 = p->use_nccl ? p->sh[0].g.voxel0 : 0;
+  for (int i = 0; i < p->nshards; ++i) {
+    Shard& s = p->sh[i];
+    if (s.g.n_local == 0) continue;
+    CK(cudaSetDevice(s.device));
+    if (!s.u0_aos) {
+      int rc = dalloc(p, s, &s.u0_aos, (size_t)s.g.n_local * p->c);
+      if (rc) return rc;
+    }
+    CK(cudaMemcpyAsync(s.u0_aos, u0 + (s.g.voxel0 - host0) * p->c,
+                       sizeof(double) * s.g.n_local * p->c, cudaMemcpyHostToDevice, s.stream));
+  }
+  for (int i = 0; i < p->nshards; ++i) {
+    CK(cudaSetDevice(p->sh[i].device));
+    CK(cudaStreamSynchronize(p->sh[i].stream));
+  }
+  p->init_src = 2;
+  return FCM_OK;
+}
+
+int fcm_run(fcm_plan* p, double m, double eps, int32_t max_iters, double* v_out,
+            double* trace_out, int32_t* iterations, int32_t* converged, int32_t* dead_cluster) {
+  if (check_plan(p)) return FCM_E_ARG;
+  p->run_ok = false;
+  if (!(m > 1.0) || !std::isfinite(m)) return fail(p, FCM_E_ARG, "fuzzifier must be > 1");
+  if (!(eps > 0.0 && eps < 1.0)) return fail(p, FCM_E_ARG, "epsilon must lie in (0, 1)");
+  if (max_iters < 1) return fail(p, FCM_E_ARG, "max_iters must be >= 1");
+  if (!p->x_ready) return fail(p, FCM_E_STATE, "fcm_upload_pixels has not been called");
+  if (!p->init_src) return fail(p, FCM_E_STATE, "no initial membership (init or upload)");
+  set_powers(p, m);
+
+  Control tmpl;
+  memset(&tmpl, 0, sizeof tmpl);
+  tmpl.dead = -1;
+  *p->host_tmpl = tmpl;
+  for (int i = 0; i < p->nshards; ++i) {
+    Shard& s = p->sh[i];
+    CK(cudaSetDevice(s.device));
+    if (s.trace_cap < max_iters) {
+      int rc = dalloc(p, s, &s.trace, (size_t)max_iters);
+      if (rc) return rc;
+      s.trace_cap = max_iters;
+    }
+    CK(cudaMemcpyAsync(s.ctl, p->host_tmpl, sizeof(Control), cudaMemcpyHostToDevice, s.stream));
+    CK(cudaMemsetAsync(s.group_cnt, 0, sizeof(unsigned) * s.g.noct * s.g.gpo, s.stream));
+    CK(cudaMemsetAsync(s.oct_cnt, 0, sizeof(unsigned) * s.g.noct, s.stream));
+  }
+  Shard& s0 = p->sh[0];
+  CK(cudaSetDevice(s0.device));
+  p->passes_launched = 0;
+  CK(cudaEventRecord(p->ev_start, s0.stream));
+  int rc = step(p, 0, eps, max_iters);
+  if (rc) return rc;
+  CK(cudaSetDevice(s0.device));
+  CK(cudaEventRecord(p->ev_pro, s0.stream));
+  int seq = 1;
+  while (seq <= max_iters) {
+    const int nb = std::min(p->batch, max_iters - seq + 1);
+    for (int b = 0; b < nb; ++b, ++seq)
+      if ((rc = step(p, seq, eps, max_iters))) return rc;
+    CK(cudaSetDevice(s0.device));
+    CK(cudaMemcpyAsync(p->host_ctl, s0.ctl, sizeof(Control), cudaMemcpyDeviceToHost, s0.stream));
+    CK(cudaStreamSynchronize(s0.stream));
+    if (p->host_ctl->done) break;
+  }
+  CK(cudaSetDevice(s0.device));
+  CK(cudaEventRecord(p->ev_end, s0.stream));
+  for (int i = 0; i < p->nshards; ++i) {
+    CK(cudaSetDevice(p->sh[i].device));
+    CK(cudaStreamSynchronize(p->sh[i].stream));
+  }
+  CK(cudaSetDevice(s0.device));
+  CK(cudaMemcpy(p->host_ctl, s0.ctl, sizeof(Control), cudaMemcpyDeviceToHost));
+  const Control& h = *p->host_ctl;
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, p->ev_start, p->ev_end));
+  p->t_loop_ms = ms;
+  CK(cudaEventElapsedTime(&ms, p->ev_start, p->ev_pro));
+  p->t_pro_ms = ms;
+  p->passes_done = h.iter;
+  p->t_pass_ms = 0;
+  if (p->timing && h.iter > 0) {
+    double tot = 0;
+    for (int k = 0; k < h.iter && k < (int)p->ev_t0.size(); ++k) {
+      CK(cudaEventElapsedTime(&ms, p->ev_t0[k], p->ev_t1[k]));
+      tot += ms;
+    }
+    p->t_pass_ms = tot / h.iter;
+  }
+  if (iterations) *iterations = h.iter;
+  if (converged) *converged = h.converged;
+  if (dead_cluster) *dead_cluster = h.dead;
+  if (v_out) memcpy(v_out, h.v, sizeof(double) * p->c);
+  if (trace_out && h.iter > 0)
+    CK(cudaMemcpy(trace_out, s0.trace, sizeof(double) * h.iter, cudaMemcpyDeviceToHost));
+  if (!h.done) return fail(p, FCM_E_STATE, "loop ended without the done flag");
+  if (h.dead >= 0) return fail(p, FCM_E_DEGENERATE, "cluster %d has zero total membership weight", h.dead);
+  p->run_ok = true;
+  return FCM_OK;
+}
+
+int fcm_download(fcm_plan* p, double* u_out, int32_t* labels_out) {
+  if (check_plan(p)) return FCM_E_ARG;
+  if (!p->run_ok) return fail(p, FCM_E_STATE, "no successful fcm_run to download");
+  const int64_t host0 = p->use_nccl ? p->sh[0].g.voxel0 : 0;
+  for (int i = 0; i < p->nshards; ++i) {
+    Shard& s = p->sh[i];
+    if (s.g.n_local == 0) continue;
+    CK(cudaSetDevice(s.device));
+    int rc;
+    if (u_out && !s.out_u && (rc = dalloc(p, s, &s.out_u, (size_t)s.g.n_local * p->c))) return rc;
+    if (labels_out && !s.out_labels && (rc = dalloc(p, s, &s.out_labels, (size_t)s.g.n_local)))
+      return rc;
+    EpilogueArgs e{};
+    e.x = s.x;
+    e.n = s.g.n_local;
+    e.c = p->c;
+    e.v = s.ctl->v;
+    e.m = p->pw.m;
+    e.p = p->pw.p;
+    e.pkind = p->pw.pkind;
+    e.pint = p->pw.pint;
+    e.mkind = p->pw.mkind;
+    e.mint = p->pw.mint;
+    e.u_out = u_out ? s.out_u : nullptr;
+    e.labels = labels_out ? s.out_labels : nullptr;
+    CK(launch_epilogue(p->xkind, p->c, p->mode, e, s.sms, s.stream));
+    if (u_out)
+      CK(cudaMemcpyAsync(u_out + (s.g.voxel0 - host0) * p->c, s.out_u,
+                         sizeof(double) * s.g.n_local * p->c, cudaMemcpyDeviceToHost, s.stream));
+    if (labels_out)
+      CK(cudaMemcpyAsync(labels_out + (s.g.voxel0 - host0), s.out_labels,
+                         sizeof(int32_t) * s.g.n_local, cudaMemcpyDeviceToHost, s.stream));
+  }
+  for (int i = 0; i < p->nshards; ++i) {
+    CK(cudaSetDevice(p->sh[i].device));
+    CK(cudaStreamSynchronize(p->sh[i].stream));
+  }
+  return FCM_OK;
+}
+
+int fcm_last_timing(const fcm_plan* p, double* out, int32_t count) {
+  if (!p || !out) return FCM_E_ARG;
+  const double v[] = {p->t_loop_ms, p->t_pass_ms, p->t_pro_ms, (double)p->passes_launched,
+                      (double)p->passes_done};
+  for (int i = 0; i < count && i < (int)(sizeof v / sizeof v[0]); ++i) out[i] = v[i];
+  return FCM_OK;
+}
+
+int fcm_host_register(void* ptr, int64_t bytes) {
+  if (!ptr || bytes <= 0) return FCM_E_ARG;
+  cudaError_t e = cudaHostRegister(ptr, (size_t)bytes, cudaHostRegisterDefault);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return FCM_E_CUDA;
+  }
+  return FCM_OK;
+}
+
+int fcm_host_unregister(void* ptr) {
+  if (!ptr) return FCM_E_ARG;
+  cudaError_t e = cudaHostUnregister(ptr);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return FCM_E_CUDA;
+  }
+  return FCM_OK;
+}
+
+// ----------------------------------------------------------- kernel seam --
+namespace {
+struct DevBuf {
+  void* p = nullptr;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+};
+#define CKS(expr)                  \
+  do {                             \
+    if ((expr) != cudaSuccess) {   \
+      cudaGetLastError();          \
+      return FCM_E_CUDA;           \
+    }                              \
+  } while (0)
+}  // namespace
+
+int fcm_fill_membership_random(double* u_out, int64_t n, int32_t c, uint64_t seed, int32_t device) {
+  if (!u_out || n < 1 || c < 1 || c > kCMaxSupported) return FCM_E_ARG;
+  CKS(cudaSetDevice(device));
+  DevBuf d;
+  CKS(cudaMalloc(&d.p, sizeof(double) * n * c));
+  CKS(op_init_aos((double*)d.p, n, c, seed, 0));
+  CKS(cudaMemcpy(u_out, d.p, sizeof(double) * n * c, cudaMemcpyDeviceToHost));
+  return FCM_OK;
+}
+
+int fcm_update_centers(const double* x, const double* u, double* v_out, int64_t n, int32_t c,
+                       double m, int32_t device, int32_t* dead_out) {
+  if (!x || !u || !v_out || n < 1 || c < 1 || c > kCMaxSupported || !(m > 1.0)) return FCM_E_ARG;
+  // One plan, prologue only: the same fused sums the loop uses for v_1.
+  // c == 1 is legal here (the reference's tests use a 1-column membership),
+  // so the plan is built for c >= 2 with zero padding columns ignored.
+  fcm_plan* p = nullptr;
+  const int cp = c < 2 ? 2 : c;
+  int rc = fcm_plan_create(&p, std::max<int64_t>(n, cp), cp, FCM_X_F64, 1, &device);
+  if (rc) return rc;
+  std::vector<double> xx(x, x + n), uu;
+  const double* up = u;
+  if (c != cp || n < cp) {
+    const int64_t nn = std::max<int64_t>(n, cp);
+    xx.assign(nn, 0.0);
+    std::copy(x, x + n, xx.begin());
+    uu.assign(nn * cp, 0.0);
+    for (int64_t i = 0; i < n; ++i)
+      for (int j = 0; j < c; ++j) uu[i * cp + j] = u[i * c + j];
+    for (int j = c; j < cp; ++j) uu[j] = 1.0;  // keep padding columns alive
+    up = uu.data();
+    if (n < nn) {
+      // padding voxels must not contribute: give them zero membership
+      for (int64_t i = n; i < nn; ++i)
+        for (int j = 0; j < cp; ++j) uu[i * cp + j] = 0.0;
+    }
+  }
+  rc = fcm_upload_pixels(p, xx.data());
+  if (!rc) rc = fcm_upload_membership(p, up);
+  if (!rc) {
+    set_powers(p, m);
+    Control tmpl;
+    memset(&tmpl, 0, sizeof tmpl);
+    tmpl.dead = -1;
+    Shard& s = p->sh[0];
+    cudaSetDevice(s.device);
+    if (s.trace_cap < 1) rc = dalloc(p, s, &s.trace, 1), s.trace_cap = 1;
+    if (!rc) {
+      *p->host_tmpl = tmpl;
+      cudaMemcpyAsync(s.ctl, p->host_tmpl, sizeof tmpl, cudaMemcpyHostToDevice, s.stream);
+      cudaMemsetAsync(s.group_cnt, 0, sizeof(unsigned) * s.g.noct * s.g.gpo, s.stream);
+      cudaMemsetAsync(s.oct_cnt, 0, sizeof(unsigned) * s.g.noct, s.stream);
+      rc = step(p, 0, 0.5, 1);
+      if (!rc && cudaStreamSynchronize(s.stream) != cudaSuccess) rc = FCM_E_CUDA;
+    }
+    if (!rc) {
+      Control h;
+      if (cudaMemcpy(&h, s.ctl, sizeof h, cudaMemcpyDeviceToHost) != cudaSuccess) rc = FCM_E_CUDA;
+      else {
+        int dead = -1;
+        for (int j = 0; j < c; ++j)
+          if (h.root[cp + j] == 0.0) { dead = j; break; }
+        if (dead_out) *dead_out = dead;
+        for (int j = 0; j < c && (dead < 0 || j < dead); ++j) v_out[j] = h.root[j] / h.root[cp + j];
+      }
+    }
+  }
+  fcm_plan_destroy(p);
+  return rc;
+}
+
+int fcm_update_membership(const double* x, const double* v, double* u_out, int64_t n, int32_t c,
+                          double m, int32_t device) {
+  if (!x || !v || !u_out || n < 1 || c < 1 || c > kCMaxSupported || !(m > 1.0)) return FCM_E_ARG;
+  CKS(cudaSetDevice(device));
+  fcm_plan tmp;  // only for powers
+  set_powers(&tmp, m);
+  DevBuf dx, dv, du;
+  CKS(cudaMalloc(&dx.p, sizeof(double) * n));
+  CKS(cudaMalloc(&dv.p, sizeof(double) * c));
+  CKS(cudaMalloc(&du.p, sizeof(double) * n * c));
+  CKS(cudaMemcpy(dx.p, x, sizeof(double) * n, cudaMemcpyHostToDevice));
+  CKS(cudaMemcpy(dv.p, v, sizeof(double) * c, cudaMemcpyHostToDevice));
+  EpilogueArgs e{};
+  e.x = dx.p;
+  e.n = n;
+  e.c = c;
+  e.v = (const double*)dv.p;
+  e.m = tmp.pw.m;
+  e.p = tmp.pw.p;
+  e.pkind = tmp.pw.pkind;
+  e.pint = tmp.pw.pint;
+  e.mkind = tmp.pw.mkind;
+  e.mint = tmp.pw.mint;
+  e.u_out = (double*)du.p;
+  e.labels = nullptr;
+  if (c == 1) {
+    // single cluster: every voxel belongs fully (or equally on a tie) to it
+    std::vector<double> ones(n, 1.0);
+    memcpy(u_out, ones.data(), sizeof(double) * n);
+    return FCM_OK;
+  }
+  CKS(launch_epilogue(XK_F64, c, tmp.mode, e, 148, 0));
+  CKS(cudaMemcpy(u_out, du.p, sizeof(double) * n * c, cudaMemcpyDeviceToHost));
+  return FCM_OK;
+}
+
+int fcm_objective(const double* x, const double* u, const double* v, int64_t n, int32_t c,
+                  double m, int32_t device, double* out) {
+  if (!x || !u || !v || !out || n < 1 || c < 1) return FCM_E_ARG;
+  CKS(cudaSetDevice(device));
+  DevBuf dx, du, dv, ds;
+  CKS(cudaMalloc(&dx.p, sizeof(double) * n));
+  CKS(cudaMalloc(&du.p, sizeof(double) * n * c));
+  CKS(cudaMalloc(&dv.p, sizeof(double) * c));
+  CKS(cudaMalloc(&ds.p, sizeof(double) * (kOpsScratch + 1)));
+  CKS(cudaMemcpy(dx.p, x, sizeof(double) * n, cudaMemcpyHostToDevice));
+  CKS(cudaMemcpy(du.p, u, sizeof(double) * n * c, cudaMemcpyHostToDevice));
+  CKS(cudaMemcpy(dv.p, v, sizeof(double) * c, cudaMemcpyHostToDevice));
+  double* s = (double*)ds.p;
+  CKS(op_reduce(0, (double*)dx.p, (double*)du.p, (double*)dv.p, n, c, m, nullptr, nullptr, s,
+                s + kOpsScratch, 0));
+  CKS(cudaMemcpy(out, s + kOpsScratch, sizeof(double), cudaMemcpyDeviceToHost));
+  return FCM_OK;
+}
+
+int fcm_max_abs_diff(const double* a, const double* b, int64_t count, int32_t device, double* out) {
+  if (!a || !b || !out || count < 0) return FCM_E_ARG;
+  if (count == 0) {
+    *out = 0.0;
+    return FCM_OK;
+  }
+  CKS(cudaSetDevice(device));
+  DevBuf da, db, ds;
+  CKS(cudaMalloc(&da.p, sizeof(double) * count));
+  CKS(cudaMalloc(&db.p, sizeof(double) * count));
+  CKS(cudaMalloc(&ds.p, sizeof(double) * (kOpsScratch + 1)));
+  CKS(cudaMemcpy(da.p, a, sizeof(double) * count, cudaMemcpyHostToDevice));
+  CKS(cudaMemcpy(db.p, b, sizeof(double) * count, cudaMemcpyHostToDevice));
+  double* s = (double*)ds.p;
+  CKS(op_reduce(1, nullptr, nullptr, nullptr, count, 0, 0.0, (double*)da.p, (double*)db.p, s,
+                s + kOpsScratch, 0));
+  CKS(cudaMemcpy(out, s + kOpsScratch, sizeof(double), cudaMemcpyDeviceToHost));
+  return FCM_OK;
+}
+
+int fcm_argmax_rows(const double* u, int32_t* labels_out, int64_t n, int32_t c, int32_t device) {
+  if (!u || !labels_out || n < 1 || c < 1) return FCM_E_ARG;
+  CKS(cudaSetDevice(device));
+  DevBuf du, dl;
+  CKS(cudaMalloc(&du.p, sizeof(double) * n * c));
+  CKS(cudaMalloc(&dl.p, sizeof(int32_t) * n));
+  CKS(cudaMemcpy(du.p, u, sizeof(double) * n * c, cudaMemcpyHostToDevice));
+  CKS(op_argmax((double*)du.p, (int32_t*)dl.p, n, c, 0));
+  CKS(cudaMemcpy(labels_out, dl.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost));
+  return FCM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,479 @@
+// fcm_kernels.cuh -- the B200 FCM loop: one fused streaming pass per iteration.
+//
+// Replaces the reference's per-iteration sequence (core._iterate,
+// core.py:105-132; parallel._iterate, parallel.py:257-331):
+//     v_k  = centers(u_{k-1})          (update_centers_linear, _kernels.pyx:72-90)
+//     u_k  = membership(x, v_k)        (update_membership_range, :93-120)
+//     d_k  = max |u_k - u_{k-1}|       (max_abs_diff, :211-220)
+//     J_k  = objective(x, u_k, v_k)    (objective_linear, :178-191)
+// with ONE kernel per iteration that reads x and u_{k-1} (fp32 SoA), writes
+// u_k (fp32 SoA), and reduces the 2c+2 doubles {sum u_k^m x, sum u_k^m, J_k,
+// d_k} through a fixed tile tree.  The CTA that completes the tree computes
+// v_{k+1} (the "finalize" step) so the next pass needs no host round trip.
+#pragma once
+#include <algorithm>
+#include <cstdio>
+
+#include "fcm_device.cuh"
+#include "fcm_kernels.h"
+
+namespace fcm {
+
+template <int NF>
+struct SmemRedT {
+  double w[kWarps][NF];
+  double root[NF];
+  int tile;
+  int flag;
+};
+using SmemRed = SmemRedT<kNFMax>;
+
+// Barrier over the kThreads reduction threads: the whole CTA for the plain
+// kernels, the consumer warps (named barrier 1) for the TMA pipeline whose
+// producer warp never joins.
+template <bool NAMED>
+__device__ __forceinline__ void red_sync() {
+  if (NAMED) asm volatile("bar.sync 1, %0;" ::"n"(kThreads) : "memory");
+  else __syncthreads();
+}
+
+// Register slot s (0..2C+1) -> payload field for runtime c <= C.
+template <int C>
+__device__ __forceinline__ int field_of(int s, int c) {
+  if (s < C) return s < c ? s : -1;
+  if (s < 2 * C) return (s - C) < c ? c + (s - C) : -1;
+  return s == 2 * C ? 2 * c : 2 * c + 1;
+}
+
+// ----------------------------------------------------------- finalize -----
+// Consumes the global root of pass k (or of the prologue) and prepares the
+// centers of the next pass; mirrors the control flow of core._iterate.
+__device__ inline void finalize(Control* ctl, const double* root, int c, double eps, int max_iters,
+                         double* trace, bool prologue) {
+  const int nf = 2 * c + 2;
+  for (int f = 0; f < nf; ++f) ctl->root[f] = root[f];
+  if (!prologue) {
+    const int k = ctl->iter + 1;
+    ctl->iter = k;
+    trace[k - 1] = root[2 * c];
+    ctl->delta = root[2 * c + 1];
+    if (root[2 * c + 1] < eps) {  // core.py:129-131
+      ctl->converged = 1;
+      ctl->done = 1;
+      return;
+    }
+    if (k >= max_iters) {  // core.py:120
+      ctl->done = 1;
+      return;
+    }
+  }
+  for (int j = 0; j < c; ++j) {  // core.py:121-123 -> DegenerateClusterError(j)
+    if (root[c + j] == 0.0) {
+      ctl->dead = j;
+      ctl->done = 1;
+      return;
+    }
+  }
+  for (int j = 0; j < c; ++j) ctl->v[j] = root[j] / root[c + j];
+}
+
+// ----------------------------------------------------------- tile tree ----
+// Reduce the per-thread payload of local tile lt to the tile partial, then
+// climb the tree: the CTA that completes a group of 32 tiles reduces the
+// group, the one that completes an octant reduces the octant, the one that
+// completes the rank reduces the rank (and finalizes when it is alone).
+template <int C, bool NAMED = false, typename SM>
+__device__ __forceinline__ void tile_finish(const PassArgs& a, int lt, const double* acc, SM& sm,
+                            bool prologue) {
+  constexpr int NS = 2 * C + 2;
+  const int c = C <= 8 ? C : a.c, nf = 2 * c + 2;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const Geometry& g = a.g;
+
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    double r = warp_tree(acc[s], s == NS - 1);
+    int f = field_of<C>(s, c);
+    if (lane == 0 && f >= 0) sm.w[warp][f] = r;
+  }
+  red_sync<NAMED>();
+  if (tid < nf) {
+    const bool mx = tid == nf - 1;
+    double q0 = combine(sm.w[0][tid], sm.w[1][tid], mx), q1 = combine(sm.w[2][tid], sm.w[3][tid], mx);
+    double q2 = combine(sm.w[4][tid], sm.w[5][tid], mx), q3 = combine(sm.w[6][tid], sm.w[7][tid], mx);
+    a.tile_part[(int64_t)lt * nf + tid] = combine(combine(q0, q1, mx), combine(q2, q3, mx), mx);
+  }
+  __threadfence();
+  red_sync<NAMED>();
+
+  const int gt = g.tile0 + lt;
+  const int oct = gt / g.M;
+  const int grp = (gt - oct * g.M) / kGroup;
+  const int loct = oct - g.oct0;
+  const int lgrp = loct * g.gpo + grp;
+  if (tid == 0) {
+    unsigned prev = atomicAdd(&a.group_cnt[lgrp], 1u);
+    sm.flag = (int)prev == group_real_tiles(g, oct, grp) - 1;
+  }
+  red_sync<NAMED>();
+  if (!sm.flag) return;
+
+  if (warp == 0) {
+    if (lane == 0) a.group_cnt[lgrp] = 0u;
+    __threadfence();
+    const int leaf = grp * kGroup + lane;
+    const bool real = leaf < g.M && (int64_t)oct * g.M + leaf < g.T;
+    const int64_t lt_leaf = (int64_t)oct * g.M + leaf - g.tile0;
+    for (int f = 0; f < nf; ++f) {
+      double v = real ? __ldcg(&a.tile_part[lt_leaf * nf + f]) : 0.0;
+      v = warp_tree(v, f == nf - 1);
+      if (lane == 0) a.group_root[(int64_t)lgrp * nf + f] = v;
+    }
+  }
+  __threadfence();
+  red_sync<NAMED>();
+  if (tid == 0) {
+    unsigned prev = atomicAdd(&a.oct_cnt[loct], 1u);
+    sm.flag = (int)prev == octant_real_groups(g, oct) - 1;
+  }
+  red_sync<NAMED>();
+  if (!sm.flag) return;
+
+  if (warp == 0) {
+    if (lane == 0) a.oct_cnt[loct] = 0u;
+    __threadfence();
+    const bool real = lane < g.gpo && group_real_tiles(g, oct, lane) > 0;
+    for (int f = 0; f < nf; ++f) {
+      double v = real ? __ldcg(&a.group_root[((int64_t)loct * g.gpo + lane) * nf + f]) : 0.0;
+      v = warp_tree(v, f == nf - 1);
+      if (lane == 0) a.oct_root[loct * nf + f] = v;
+    }
+  }
+  __threadfence();
+  red_sync<NAMED>();
+  if (tid == 0) {
+    unsigned prev = atomicAdd(&a.ctl->rank_cnt, 1u);
+    sm.flag = (int)prev == rank_real_octants(g) - 1;
+  }
+  red_sync<NAMED>();
+  if (!sm.flag) return;
+
+  if (warp == 0) {
+    if (lane == 0) a.ctl->rank_cnt = 0u;
+    __threadfence();
+    const bool real = lane < g.noct && (int64_t)(g.oct0 + lane) * g.M < g.T;
+    for (int f = 0; f < nf; ++f) {
+      double v = real ? __ldcg(&a.oct_root[lane * nf + f]) : 0.0;
+      v = warp_tree(v, f == nf - 1);
+      if (lane == 0) {
+        a.rank_root[f] = v;
+        sm.root[f] = v;
+      }
+    }
+    if (lane == 0 && g.nranks == 1)
+      finalize(a.ctl, sm.root, c, a.eps, a.max_iters, a.trace, prologue);
+    __threadfence();
+  }
+}
+
+// ---------------------------------------------------------------- loads ---
+template <typename XT>
+struct XLoad;
+template <>
+struct XLoad<uint8_t> {
+  static __device__ __forceinline__ void load4(const uint8_t* x, int64_t i, double* xd) {
+    unsigned w = __ldg(reinterpret_cast<const unsigned*>(x + i));
+#pragma unroll
+    for (int q = 0; q < 4; ++q) xd[q] = (double)((w >> (8 * q)) & 0xffu);
+  }
+  static __device__ __forceinline__ double load1(const uint8_t* x, int64_t i) { return (double)x[i]; }
+};
+template <>
+struct XLoad<double> {
+  static __device__ __forceinline__ void load4(const double* x, int64_t i, double* xd) {
+    double2 a = __ldg(reinterpret_cast<const double2*>(x + i));
+    double2 b = __ldg(reinterpret_cast<const double2*>(x + i + 2));
+    xd[0] = a.x;
+    xd[1] = a.y;
+    xd[2] = b.x;
+    xd[3] = b.y;
+  }
+  static __device__ __forceinline__ double load1(const double* x, int64_t i) { return x[i]; }
+};
+
+__device__ __forceinline__ float f4get(const float4& v, int q) {
+  return q == 0 ? v.x : q == 1 ? v.y : q == 2 ? v.z : v.w;
+}
+__device__ __forceinline__ void f4set(float4& v, int q, float s) {
+  if (q == 0) v.x = s;
+  else if (q == 1) v.y = s;
+  else if (q == 2) v.z = s;
+  else v.w = s;
+}
+
+__device__ __forceinline__ Powers load_powers(const PassArgs& a) {
+  Powers p;
+  p.m = a.m;
+  p.p = a.p;
+  p.pkind = a.pkind;
+  p.pint = a.pint;
+  p.mkind = a.mkind;
+  p.mint = a.mint;
+  return p;
+}
+
+// ------------------------------------------------------------ the pass ----
+// Four voxels per thread per step; u planes move as float4 (128-bit) loads
+// and stores, x as one 32-bit (u8) / 64-bit (u16) / 2x128-bit (f64) load.
+template <typename XT, int C, int MODE, bool MASK>
+__device__ __forceinline__ void pass_tile(const PassArgs& a, int lt, const double* v,
+                                          const Powers& pw, double* acc) {
+  const int c = a.c;
+  const int64_t base = (int64_t)lt << a.g.tile_shift;
+  const int steps = (1 << a.g.tile_shift) / (kThreads * kVec);
+  const float* __restrict__ ucur = a.u_cur;
+  float* __restrict__ unxt = a.u_nxt;
+  const int64_t plane = a.g.plane;
+#pragma unroll 1
+  for (int r = 0; r < steps; ++r) {
+    const int64_t i0 = base + ((int64_t)r * kThreads + threadIdx.x) * kVec;
+    if (MASK && i0 >= a.g.n_local) break;
+    double xd[4];
+    XLoad<XT>::load4(reinterpret_cast<const XT*>(a.x), i0, xd);
+    float4 uo[C], un[C];
+#pragma unroll
+    for (int j = 0; j < C; ++j)
+      if (j < c) uo[j] = __ldcs(reinterpret_cast<const float4*>(ucur + j * plane + i0));
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      double u[C];
+      membership<C, MODE>(xd[q], v, c, pw, u);
+      const bool valid = !MASK || (i0 + q < a.g.n_local);
+#pragma unroll
+      for (int j = 0; j < C; ++j) {
+        if (j < c) {
+          const double w = pow_m<MODE>(u[j], pw);
+          const double dj = xd[q] - v[j];
+          const double dl = fabs(u[j] - (double)f4get(uo[j], q));
+          if (valid) {
+            acc[j] = fma(w, xd[q], acc[j]);
+            acc[C + j] += w;
+            acc[2 * C] = fma(w, dj * dj, acc[2 * C]);
+            acc[2 * C + 1] = fmax(acc[2 * C + 1], dl);
+          }
+          f4set(un[j], q, (float)u[j]);
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < C; ++j)
+      if (j < c) __stcs(reinterpret_cast<float4*>(unxt + j * plane + i0), un[j]);
+  }
+}
+
+template <typename XT, int C, int MODE>
+__global__ void __launch_bounds__(kThreads) pass_kernel(PassArgs a) {
+  __shared__ SmemRed sm;
+  if (threadIdx.x == 0) sm.flag = *(volatile int*)&a.ctl->done;
+  __syncthreads();
+  if (sm.flag) return;
+  if (blockIdx.x == 0 && threadIdx.x == 0) a.ctl->tile_next[(a.seq + 1) & 1] = 0u;
+  double v[C];
+#pragma unroll
+  for (int j = 0; j < C; ++j) v[j] = j < a.c ? a.ctl->v[j] : 0.0;
+  const Powers pw = load_powers(a);
+  const int ntiles = a.g.tiles_local;
+  for (;;) {
+    if (threadIdx.x == 0) sm.tile = (int)atomicAdd(&a.ctl->tile_next[a.seq & 1], 1u);
+    __syncthreads();
+    const int lt = sm.tile;
+    __syncthreads();
+    if (lt >= ntiles) break;
+    double acc[2 * C + 2];
+#pragma unroll
+    for (int s = 0; s < 2 * C + 2; ++s) acc[s] = 0.0;
+    const bool full = ((int64_t)(lt + 1) << a.g.tile_shift) <= a.g.n_local;
+    if (full) pass_tile<XT, C, MODE, false>(a, lt, v, pw, acc);
+    else pass_tile<XT, C, MODE, true>(a, lt, v, pw, acc);
+    tile_finish<C>(a, lt, acc, sm, false);
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------ prologue ----
+// Builds u_0 (fp32 SoA, for delta_1) and the sums of u_0^m x / u_0^m that
+// give v_1, from either the seeded generator (bit-exact with
+// core.init_membership) or an uploaded fp64 AoS initial membership.
+template <typename XT, int C, int MODE, bool FROM_SEED>
+__global__ void __launch_bounds__(kThreads) prologue_kernel(PassArgs a) {
+  __shared__ SmemRed sm;
+  if (threadIdx.x == 0) sm.flag = *(volatile int*)&a.ctl->done;
+  __syncthreads();
+  if (sm.flag) return;
+  if (blockIdx.x == 0 && threadIdx.x == 0) a.ctl->tile_next[(a.seq + 1) & 1] = 0u;
+  const Powers pw = load_powers(a);
+  const int c = a.c;
+  const int ntiles = a.g.tiles_local;
+  for (;;) {
+    if (threadIdx.x == 0) sm.tile = (int)atomicAdd(&a.ctl->tile_next[a.seq & 1], 1u);
+    __syncthreads();
+    const int lt = sm.tile;
+    __syncthreads();
+    if (lt >= ntiles) break;
+    double acc[2 * C + 2];
+#pragma unroll
+    for (int s = 0; s < 2 * C + 2; ++s) acc[s] = 0.0;
+    const int64_t base = (int64_t)lt << a.g.tile_shift;
+    const int steps = (1 << a.g.tile_shift) / (kThreads * kVec);
+    for (int r = 0; r < steps; ++r) {
+      const int64_t i0 = base + ((int64_t)r * kThreads + threadIdx.x) * kVec;
+      if (i0 >= a.g.n_local) break;
+      double xd[4];
+      XLoad<XT>::load4(reinterpret_cast<const XT*>(a.x), i0, xd);
+      float4 un[C];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int64_t i = i0 + q;
+        const bool valid = i < a.g.n_local;
+        double u[C];
+        if (FROM_SEED) {
+          init_row<C>(a.seed, a.g.voxel0 + i, c, u);
+        } else {
+#pragma unroll
+          for (int j = 0; j < C; ++j) u[j] = (j < c && valid) ? a.u0_aos[i * c + j] : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < C; ++j) {
+          if (j < c) {
+            if (valid) {
+              const double w = pow(u[j], a.m);  // exactly the reference's pow(u, m)
+              acc[j] = fma(w, xd[q], acc[j]);
+              acc[C + j] += w;
+            }
+            f4set(un[j], q, (float)u[j]);
+          }
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < C; ++j)
+        if (j < c) *reinterpret_cast<float4*>(a.u_nxt + j * a.g.plane + i0) = un[j];
+    }
+    tile_finish<C>(a, lt, acc, sm, true);
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------ epilogue ----
+// u_final = membership(x, v_final) in fp64 AoS (what the reference returns,
+// core.py:132) and labels = argmax with ties to the lowest index.
+template <typename XT, int C, int MODE>
+__global__ void __launch_bounds__(kThreads) epilogue_kernel(EpilogueArgs a) {
+  double v[C];
+#pragma unroll
+  for (int j = 0; j < C; ++j) v[j] = j < a.c ? a.v[j] : 0.0;
+  Powers pw;
+  pw.m = a.m; pw.p = a.p; pw.pkind = a.pkind; pw.pint = a.pint; pw.mkind = a.mkind; pw.mint = a.mint;
+  const int c = a.c;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double xd = XLoad<XT>::load1(reinterpret_cast<const XT*>(a.x), i);
+    double u[C];
+    membership<C, MODE>(xd, v, c, pw, u);
+    if (a.u_out) {
+#pragma unroll
+      for (int j = 0; j < C; ++j)
+        if (j < c) a.u_out[i * c + j] = u[j];
+    }
+    if (a.labels) {
+      double best = u[0];
+      int bj = 0;
+#pragma unroll
+      for (int j = 1; j < C; ++j)
+        if (j < c && u[j] > best) {
+          best = u[j];
+          bj = j;
+        }
+      a.labels[i] = bj;
+    }
+  }
+}
+
+}  // namespace fcm
+#include "fcm_pass_tma.cuh"
+namespace fcm {
+
+// ------------------------------------------------------------ launchers ---
+template <typename KernelPtr>
+inline int occupancy_grid(KernelPtr k, int tiles, int sms) {
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, 0);
+  if (per_sm < 1) per_sm = 1;
+  long long g = (long long)per_sm * sms;
+  if (g > tiles) g = tiles;
+  return g < 1 ? 1 : (int)g;
+}
+
+// One translation unit per cluster count C instantiates these (fcm_inst_c*.cu).
+template <int C>
+cudaError_t launch_pass_c(int xkind, int mode, const PassArgs& a, int sms, cudaStream_t st,
+                          int* grid_out, int variant, int force_grid) {
+  constexpr int MD = C <= 8 ? MODE_M2 : MODE_GEN;
+  const bool m2 = (mode == MODE_M2) && C <= 8;
+  if (variant == 0) {  // TMA bulk pipeline (production)
+    if (xkind == XK_U8)
+      return m2 ? launch_pass_tma<uint8_t, C, MD>(a, sms, st, grid_out, force_grid)
+                : launch_pass_tma<uint8_t, C, MODE_GEN>(a, sms, st, grid_out, force_grid);
+    return m2 ? launch_pass_tma<double, C, MD>(a, sms, st, grid_out, force_grid)
+              : launch_pass_tma<double, C, MODE_GEN>(a, sms, st, grid_out, force_grid);
+  }
+  int grid = 0;  // variant 1: register-staged LDG/STG kernel (kept for A/B)
+  auto go = [&](auto k) {
+    grid = force_grid > 0 ? std::min(force_grid, a.g.tiles_local) : occupancy_grid(k, a.g.tiles_local, sms);
+    k<<<grid, kThreads, 0, st>>>(a);
+  };
+  if (xkind == XK_U8) {
+    if (m2) go(pass_kernel<uint8_t, C, MD>);
+    else go(pass_kernel<uint8_t, C, MODE_GEN>);
+  } else {
+    if (m2) go(pass_kernel<double, C, MD>);
+    else go(pass_kernel<double, C, MODE_GEN>);
+  }
+  if (grid_out) *grid_out = grid;
+  return cudaGetLastError();
+}
+
+template <int C>
+cudaError_t launch_prologue_c(int xkind, bool from_seed, const PassArgs& a, int sms, cudaStream_t st) {
+  auto go = [&](auto k) { k<<<occupancy_grid(k, a.g.tiles_local, sms), kThreads, 0, st>>>(a); };
+  if (xkind == XK_U8) {
+    if (from_seed) go(prologue_kernel<uint8_t, C, MODE_GEN, true>);
+    else go(prologue_kernel<uint8_t, C, MODE_GEN, false>);
+  } else {
+    if (from_seed) go(prologue_kernel<double, C, MODE_GEN, true>);
+    else go(prologue_kernel<double, C, MODE_GEN, false>);
+  }
+  return cudaGetLastError();
+}
+
+template <int C>
+cudaError_t launch_epilogue_c(int xkind, int mode, const EpilogueArgs& a, int sms, cudaStream_t st) {
+  long long want = (a.n + kThreads - 1) / kThreads;
+  long long cap = (long long)sms * 8;
+  int grid = (int)(want < cap ? (want < 1 ? 1 : want) : cap);
+  const bool m2 = (mode == MODE_M2) && C <= 8;
+  if (xkind == XK_U8) {
+    if (m2) epilogue_kernel<uint8_t, C, (C <= 8 ? MODE_M2 : MODE_GEN)><<<grid, kThreads, 0, st>>>(a);
+    else epilogue_kernel<uint8_t, C, MODE_GEN><<<grid, kThreads, 0, st>>>(a);
+  } else {
+    if (m2) epilogue_kernel<double, C, (C <= 8 ? MODE_M2 : MODE_GEN)><<<grid, kThreads, 0, st>>>(a);
+    else epilogue_kernel<double, C, MODE_GEN><<<grid, kThreads, 0, st>>>(a);
+  }
+  return cudaGetLastError();
+}
+
+#define FCM_INSTANTIATE(C)                                                                        \
+  template cudaError_t launch_pass_c<C>(int, int, const PassArgs&, int, cudaStream_t, int*, int, int); \
+  template cudaError_t launch_prologue_c<C>(int, bool, const PassArgs&, int, cudaStream_t);      \
+  template cudaError_t launch_epilogue_c<C>(int, int, const EpilogueArgs&, int, cudaStream_t);
+
+}  // namespace fcm

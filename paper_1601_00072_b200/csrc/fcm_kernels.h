@@ -1,0 +1,66 @@
+// fcm_kernels.h -- internal interface between the C-ABI host code and the
+// CUDA kernels (not part of the public ABI; see include/fcm_b200.h).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "fcm_device.cuh"
+
+namespace fcm {
+
+enum { XK_U8 = 0, XK_F64 = 2 };
+
+struct PassArgs {
+  const void* x;          // pixels of this rank, padded to the plane length
+  const float* u_cur;     // u_{k-1}, fp32 SoA: plane j at u_cur + j * plane
+  float* u_nxt;           // u_k
+  const double* u0_aos;   // prologue source when not seeded
+  uint64_t seed;          // prologue source when seeded
+  int c;
+  double m, p;
+  int pkind, pint, mkind, mint;
+  double eps;
+  int max_iters;
+  int seq;                // pass sequence number in this run (tile-scheduler parity)
+  Geometry g;
+  double* tile_part;      // [tiles_local][nf]
+  double* group_root;     // [noct * gpo][nf]
+  double* oct_root;       // [noct][nf]
+  double* rank_root;      // [nf]
+  unsigned* group_cnt;    // [noct * gpo]
+  unsigned* oct_cnt;      // [noct]
+  Control* ctl;
+  double* trace;          // [max_iters]
+};
+
+struct FinalizeArgs {
+  const double* roots[kOctants];  // rank r's reduction root (peer, local or NCCL-gathered)
+  int nranks, c;
+  double eps;
+  int max_iters;
+  int prologue;
+  Control* ctl;
+  double* trace;
+};
+
+struct EpilogueArgs {
+  const void* x;
+  int64_t n;
+  int c;
+  const double* v;
+  double m, p;
+  int pkind, pint, mkind, mint;
+  double* u_out;    // AoS fp64 [n][c] or null
+  int32_t* labels;  // [n] or null
+};
+
+// variant 0: TMA bulk-copy pipeline (default); 1: register-staged LDG kernel.
+cudaError_t launch_pass(int xkind, int c, int mode, const PassArgs& a, int sms, cudaStream_t st,
+                        int* grid_out, int variant = 0, int force_grid = 0);
+cudaError_t launch_prologue(int xkind, int c, bool from_seed, const PassArgs& a, int sms,
+                            cudaStream_t st);
+cudaError_t launch_epilogue(int xkind, int c, int mode, const EpilogueArgs& a, int sms,
+                            cudaStream_t st);
+cudaError_t launch_finalize(const FinalizeArgs& a, cudaStream_t st);
+
+}  // namespace fcm

@@ -1,0 +1,116 @@
+// fcm_ops.cu -- the kernel seam: single GPU ops on the reference's buffer
+// conventions (flat float64, AoS memberships), one call = one op.
+// Mirrors _kernels.pyx:44-69 (fill_membership_random), :178-191
+// (objective_linear), :211-220 (max_abs_diff), :223-238 (argmax_rows).
+// Sums use a fixed two-level tree (per-CTA chunk tree, then one CTA over the
+// partials) so every result is deterministic.
+#include "fcm_device.cuh"
+#include "fcm_ops.h"
+
+namespace fcm {
+
+constexpr int kOpsBlocks = 1024;
+
+__global__ void init_aos_kernel(double* u, int64_t n, int c, uint64_t seed) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double row[kCMaxSupported];
+    init_row<kCMaxSupported>(seed, i, c, row);
+    for (int j = 0; j < c; ++j) u[i * c + j] = row[j];
+  }
+}
+
+// Block tree: thread partials -> warp trees -> adjacent pairs over warps.
+__device__ double block_tree(double x, bool is_max) {
+  __shared__ double w[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  x = warp_tree(x, is_max);
+  if (lane == 0) w[warp] = x;
+  __syncthreads();
+  double r = 0.0;
+  if (warp == 0) {
+    r = warp_tree(lane < nw ? w[lane] : 0.0, is_max);
+  }
+  __syncthreads();
+  return r;
+}
+
+// kind 0: objective terms sum_j pow(u_ij, m) (x_i - v_j)^2 ; kind 1: |a_i - b_i| (max)
+__global__ void terms_kernel(int kind, const double* x, const double* u, const double* v, int64_t n,
+                             int c, double m, const double* a, const double* b, double* partials) {
+  const int64_t chunk = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t lo = (int64_t)blockIdx.x * chunk;
+  const int64_t hi = lo + chunk < n ? lo + chunk : n;
+  double acc = 0.0;
+  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+    if (kind == 0) {
+      double t = 0.0;
+      for (int j = 0; j < c; ++j) {
+        const double d = x[i] - v[j];
+        t += pow(u[i * c + j], m) * (d * d);
+      }
+      acc += t;
+    } else {
+      acc = fmax(acc, fabs(a[i] - b[i]));
+    }
+  }
+  const double r = block_tree(acc, kind == 1);
+  if (threadIdx.x == 0) partials[blockIdx.x] = r;
+}
+
+__global__ void partials_kernel(const double* partials, int np, bool is_max, double* out) {
+  // np <= blockDim.x * k: each thread folds a contiguous run, then the block tree.
+  double acc = 0.0;
+  const int per = (np + blockDim.x - 1) / blockDim.x;
+  for (int k = 0; k < per; ++k) {
+    const int i = threadIdx.x * per + k;
+    if (i < np) acc = is_max ? fmax(acc, partials[i]) : acc + partials[i];
+  }
+  const double r = block_tree(acc, is_max);
+  if (threadIdx.x == 0) *out = r;
+}
+
+__global__ void argmax_kernel(const double* u, int32_t* labels, int64_t n, int c) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double best = u[i * c];
+    int bj = 0;
+    for (int j = 1; j < c; ++j) {
+      const double w = u[i * c + j];
+      if (w > best) {
+        best = w;
+        bj = j;
+      }
+    }
+    labels[i] = bj;
+  }
+}
+
+static int grid_for(int64_t n) {
+  int64_t g = (n + kThreads - 1) / kThreads;
+  if (g > 148 * 16) g = 148 * 16;
+  return g < 1 ? 1 : (int)g;
+}
+
+cudaError_t op_init_aos(double* u, int64_t n, int c, uint64_t seed, cudaStream_t st) {
+  init_aos_kernel<<<grid_for(n), kThreads, 0, st>>>(u, n, c, seed);
+  return cudaGetLastError();
+}
+
+cudaError_t op_reduce(int kind, const double* x, const double* u, const double* v, int64_t n, int c,
+                      double m, const double* a, const double* b, double* scratch, double* out,
+                      cudaStream_t st) {
+  int blocks = (int)((n + 4095) / 4096);
+  if (blocks > kOpsBlocks) blocks = kOpsBlocks;
+  if (blocks < 1) blocks = 1;
+  terms_kernel<<<blocks, kThreads, 0, st>>>(kind, x, u, v, n, c, m, a, b, scratch);
+  partials_kernel<<<1, kThreads, 0, st>>>(scratch, blocks, kind == 1, out);
+  return cudaGetLastError();
+}
+
+cudaError_t op_argmax(const double* u, int32_t* labels, int64_t n, int c, cudaStream_t st) {
+  argmax_kernel<<<grid_for(n), kThreads, 0, st>>>(u, labels, n, c);
+  return cudaGetLastError();
+}
+
+}  // namespace fcm

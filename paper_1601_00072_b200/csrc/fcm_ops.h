@@ -1,0 +1,14 @@
+// fcm_ops.h -- single-op kernels behind the kernel-seam half of the C ABI.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace fcm {
+constexpr int kOpsScratch = 1024;  // doubles of scratch op_reduce needs
+cudaError_t op_init_aos(double* u, int64_t n, int c, uint64_t seed, cudaStream_t st);
+// kind 0: objective (x, u, v, m); kind 1: max |a - b| over n elements
+cudaError_t op_reduce(int kind, const double* x, const double* u, const double* v, int64_t n, int c,
+                      double m, const double* a, const double* b, double* scratch, double* out,
+                      cudaStream_t st);
+cudaError_t op_argmax(const double* u, int32_t* labels, int64_t n, int c, cudaStream_t st);
+}  // namespace fcm

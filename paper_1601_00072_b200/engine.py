@@ -1,0 +1,318 @@
+"""The GPU engine: drop-in for the reference's FCM entry points.
+
+Reference surface (fcmseg, /root/reference/pkg/src/fcmseg):
+
+* run_fcm_sequential / run_fcm_parallel (core.py:146-171, parallel.py:334-362)
+  -> run_fcm_gpu(img, cfg, devices=None, initial_membership=None), same
+  validation, same FcmResult.
+* core._iterate / parallel._iterate (core.py:105-132, parallel.py:257-331), the
+  region the reference benchmark times (bench.py:49-59) -> _iterate(x, u0, cfg,
+  devices=None) returning (v, u, iterations, trace, converged).
+* the single-step operations init_membership, update_centers,
+  update_membership, objective, membership_delta, defuzzify (core.py:24-102)
+  -> same names on the GPU.
+
+Every call goes through libfcm_b200.so (include/fcm_b200.h); nothing here
+computes on the CPU except argument validation and result packaging.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from ._lib import check, lib, ptr
+from .errors import DegenerateClusterError, DimensionMismatchError, FcmError, InvalidConfigError
+from .types import ClusterCenters, FcmConfig, FcmResult, GrayImage, LabelMap, MembershipMatrix
+
+C_MAX = 16
+
+
+def pixel_kind(pixels: np.ndarray):
+    """Pick the narrowest exact device representation of the pixels.
+
+    Integer intensities 0..255 travel and live in HBM as uint8 (every
+    BASELINE config); anything else stays float64 (types.py:38-41 accepts any
+    finite non-negative value).  Returns (FCM_X_*, contiguous array).
+    """
+    if pixels.dtype == np.uint8:
+        return _lib.FCM_X_U8, np.ascontiguousarray(pixels)
+    x = np.ascontiguousarray(pixels, dtype=np.float64)
+    if x.size and x.max() <= 255.0 and x.min() >= 0.0 and np.array_equal(x, np.rint(x)):
+        return _lib.FCM_X_U8, x.astype(np.uint8)
+    return _lib.FCM_X_F64, x
+
+
+def _devices(devices):
+    if devices is None:
+        return [0]
+    if isinstance(devices, int):
+        if devices < 1:
+            raise InvalidConfigError(f"device count must be >= 1, got {devices!r}")
+        return list(range(devices))
+    devs = [int(d) for d in devices]
+    if len(devs) not in (1, 2, 4, 8):
+        raise InvalidConfigError(f"shard count must be 1, 2, 4 or 8, got {len(devs)}")
+    return devs
+
+
+class FcmPlan:
+    """Device-resident FCM problem: pixels, memberships and reduction state.
+
+    One plan per host thread (the C plan is not re-entrant).  Single-process
+    plans shard over `devices` (repeats allowed); rank plans (FcmPlan.for_rank)
+    own one rank's voxel range of a multi-process job and exchange the
+    2c+2-double reduction roots over NCCL.
+    """
+
+    def __init__(self, n: int, c: int, x_kind: int, devices=None, _handle=None):
+        if _handle is not None:
+            self._h = _handle
+        else:
+            devs = _devices(devices)
+            arr = (ctypes.c_int32 * len(devs))(*devs)
+            h = ctypes.c_void_p()
+            check(lib().fcm_plan_create(ctypes.byref(h), int(n), int(c), int(x_kind), len(devs), arr),
+                  None, "fcm_plan_create")
+            self._h = h
+        self.n, self.c, self.x_kind = int(n), int(c), int(x_kind)
+        info = self.info()
+        self.n_local, self.voxel0 = info["n_local"], info["voxel0"]
+
+    @classmethod
+    def for_rank(cls, n_global: int, c: int, x_kind: int, device: int, nranks: int, rank: int,
+                 nccl_id: bytes | None = None):
+        h = ctypes.c_void_p()
+        idbuf = ctypes.create_string_buffer(nccl_id, 128) if nccl_id else None
+        check(lib().fcm_plan_create_rank(ctypes.byref(h), int(n_global), int(c), int(x_kind), int(device),
+                                         int(nranks), int(rank), idbuf), None, "fcm_plan_create_rank")
+        return cls(n_global, c, x_kind, _handle=h)
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = ctypes.create_string_buffer(128)
+        check(lib().fcm_nccl_unique_id(buf), None, "fcm_nccl_unique_id")
+        return buf.raw
+
+    # -- lifecycle -------------------------------------------------------
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().fcm_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # -- configuration ---------------------------------------------------
+    def set_option(self, key: int, value: int):
+        check(lib().fcm_set_option(self._h, key, int(value)), self._h, "fcm_set_option")
+
+    def info(self) -> dict:
+        keys = ("n_global", "n_local", "voxel0", "tile", "tiles", "tiles_local", "grid", "nshards", "dev_bytes")
+        buf = (ctypes.c_int64 * len(keys))()
+        check(lib().fcm_plan_info(self._h, buf, len(keys)), self._h, "fcm_plan_info")
+        return dict(zip(keys, list(buf)))
+
+    # -- data ------------------------------------------------------------
+    def upload_pixels(self, x: np.ndarray):
+        """Pixels of this plan's voxel range, uint8 (FCM_X_U8) or float64."""
+        want = np.uint8 if self.x_kind == _lib.FCM_X_U8 else np.float64
+        x = np.ascontiguousarray(x, dtype=want)
+        check(lib().fcm_upload_pixels(self._h, ptr(x)), self._h, "fcm_upload_pixels")
+
+    def init_membership(self, seed: int):
+        """Seeded SplitMix64 start, generated on the device (core.init_membership)."""
+        check(lib().fcm_init_membership(self._h, int(seed) & 0xFFFFFFFFFFFFFFFF), self._h, "fcm_init_membership")
+
+    def upload_membership(self, u0: np.ndarray):
+        """Explicit AoS float64 start (initial_membership=, core.py:135-143)."""
+        u0 = np.ascontiguousarray(u0, dtype=np.float64)
+        check(lib().fcm_upload_membership(self._h, ptr(u0)), self._h, "fcm_upload_membership")
+
+    # -- the loop --------------------------------------------------------
+    def run(self, m: float, epsilon: float, max_iters: int):
+        """Returns (v, trace, iterations, converged); raises DegenerateClusterError."""
+        v = np.zeros(self.c, dtype=np.float64)
+        trace = np.zeros(max_iters, dtype=np.float64)
+        it, conv, dead = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+        st = lib().fcm_run(self._h, float(m), float(epsilon), int(max_iters), ptr(v), ptr(trace),
+                           ctypes.byref(it), ctypes.byref(conv), ctypes.byref(dead))
+        if st == _lib.FCM_E_DEGENERATE:
+            raise DegenerateClusterError(int(dead.value))
+        check(st, self._h, "fcm_run")
+        k = int(it.value)
+        return v, trace[:k].copy(), k, bool(conv.value)
+
+    def download(self, membership: bool = True, labels: bool = True, u_out=None, labels_out=None):
+        """Final membership (AoS float64) and labels of this plan's voxel range."""
+        u = None
+        lab = None
+        if membership:
+            u = u_out if u_out is not None else np.empty(self.n_local * self.c, dtype=np.float64)
+        if labels:
+            lab = labels_out if labels_out is not None else np.empty(self.n_local, dtype=np.int32)
+        check(lib().fcm_download(self._h, ptr(u), ptr(lab)), self._h, "fcm_download")
+        return u, lab
+
+    def timing(self) -> dict:
+        keys = ("loop_ms", "pass_ms", "prologue_ms", "passes_launched", "passes")
+        buf = (ctypes.c_double * len(keys))()
+        check(lib().fcm_last_timing(self._h, buf, len(keys)), self._h, "fcm_last_timing")
+        return dict(zip(keys, list(buf)))
+
+
+# ----------------------------------------------------------------- engine --
+def _check_c(c: int):
+    if c > C_MAX:
+        raise InvalidConfigError(f"the GPU path supports c <= {C_MAX}, got {c}")
+
+
+def _iterate(x: np.ndarray, u0: np.ndarray | None, cfg: FcmConfig, devices=None, seed: int | None = None):
+    """Device counterpart of core._iterate (core.py:105-132).
+
+    x: pixels (float64 or uint8); u0: AoS float64 start, or None with `seed`
+    to generate the reference's seeded start on the device.  Returns
+    (v, u_final, iterations, trace, converged) like the reference.
+    """
+    _check_c(cfg.c)
+    kind, xx = pixel_kind(np.asarray(x))
+    n = xx.shape[0]
+    with FcmPlan(n, cfg.c, kind, devices) as plan:
+        plan.upload_pixels(xx)
+        if u0 is None:
+            plan.init_membership(cfg.seed64 if seed is None else seed)
+        else:
+            plan.upload_membership(u0)
+        v, trace, k, conv = plan.run(cfg.m, cfg.epsilon, cfg.max_iters)
+        u, _ = plan.download(membership=True, labels=False)
+    return v, u, k, list(trace), conv
+
+
+def run_fcm_gpu(img: GrayImage, cfg: FcmConfig, devices=None,
+                initial_membership: MembershipMatrix | None = None) -> FcmResult:
+    """Cluster an image on the GPU; drop-in for run_fcm_sequential / run_fcm_parallel.
+
+    Same seeded initialization as the reference engines (SplitMix64, generated
+    on the device), same convergence rule, same result contract.  `devices`
+    shards the voxels (1, 2, 4 or 8 shards; results are bit-identical for any
+    shard count, mirroring workers= invariance, parallel.py:1-11).
+    """
+    n = img.pixel_count
+    if n < cfg.c:
+        raise InvalidConfigError(f"need at least {cfg.c} pixels for {cfg.c} clusters, got {n}")
+    _check_c(cfg.c)
+    if initial_membership is not None and (initial_membership.n != n or initial_membership.c != cfg.c):
+        raise DimensionMismatchError(
+            f"initial membership is {initial_membership.n}x{initial_membership.c}, expected {n}x{cfg.c}")
+    kind, xx = pixel_kind(img.pixels)
+    with FcmPlan(n, cfg.c, kind, devices) as plan:
+        plan.upload_pixels(xx)
+        if initial_membership is None:
+            plan.init_membership(cfg.seed64)
+        else:
+            plan.upload_membership(initial_membership.u)
+        v, trace, k, conv = plan.run(cfg.m, cfg.epsilon, cfg.max_iters)
+        u, labels = plan.download()
+    return FcmResult(
+        centers=ClusterCenters(v),
+        membership=MembershipMatrix(n, cfg.c, u),
+        labels=LabelMap(img.width, img.height, labels, cfg.c),
+        iterations=k,
+        objective_trace=tuple(float(t) for t in trace),
+        converged=conv,
+    )
+
+
+ENGINES = {"gpu": run_fcm_gpu}
+
+
+# ------------------------------------------------------ single operations --
+def _require_fuzzifier(m: float) -> float:
+    m = float(m)
+    if not np.isfinite(m) or m <= 1.0:
+        raise InvalidConfigError(f"fuzzifier must be a finite real > 1, got {m!r}")
+    return m
+
+
+def init_membership(n: int, cfg: FcmConfig, device: int = 0) -> MembershipMatrix:
+    """Seeded start on the GPU, bit-identical to core.init_membership (core.py:24-39)."""
+    if not isinstance(n, int) or n < 1:
+        raise InvalidConfigError(f"pixel count must be an integer >= 1, got {n!r}")
+    _check_c(cfg.c)
+    u = np.empty(n * cfg.c, dtype=np.float64)
+    check(lib().fcm_fill_membership_random(ptr(u), n, cfg.c, cfg.seed64, device), None, "fill_membership_random")
+    matrix = MembershipMatrix(n, cfg.c, u)
+    if n > cfg.c:
+        cols = matrix.as_rows().sum(axis=0)
+        if np.any(cols <= 0.0) or np.any(cols >= n):
+            raise FcmError("randomized initialization produced an empty or saturated cluster")
+    return matrix
+
+
+def update_centers(img: GrayImage, u: MembershipMatrix, m: float, device: int = 0) -> ClusterCenters:
+    """Eq. 3 on the GPU (core.update_centers, core.py:42-57)."""
+    m = _require_fuzzifier(m)
+    if u.n != img.pixel_count:
+        raise DimensionMismatchError(f"membership covers {u.n} pixels but the image has {img.pixel_count}")
+    _check_c(u.c)
+    v = np.zeros(u.c, dtype=np.float64)
+    dead = ctypes.c_int32(-1)
+    check(lib().fcm_update_centers(ptr(img.pixels), ptr(u.u), ptr(v), u.n, u.c, m, device, ctypes.byref(dead)),
+          None, "update_centers")
+    if dead.value >= 0:
+        raise DegenerateClusterError(int(dead.value))
+    return ClusterCenters(v)
+
+
+def update_membership(img: GrayImage, v: ClusterCenters, m: float, device: int = 0) -> MembershipMatrix:
+    """Eq. 4 on the GPU (core.update_membership, core.py:60-70)."""
+    m = _require_fuzzifier(m)
+    _check_c(v.c)
+    n = img.pixel_count
+    u = np.empty(n * v.c, dtype=np.float64)
+    check(lib().fcm_update_membership(ptr(img.pixels), ptr(v.v), ptr(u), n, v.c, m, device), None,
+          "update_membership")
+    return MembershipMatrix(n, v.c, u)
+
+
+def objective(img: GrayImage, u: MembershipMatrix, v: ClusterCenters, m: float, device: int = 0) -> float:
+    """J = sum_i sum_j u_ij^m (x_i - v_j)^2 on the GPU (core.objective, core.py:73-82)."""
+    m = _require_fuzzifier(m)
+    if u.n != img.pixel_count:
+        raise DimensionMismatchError(f"membership covers {u.n} pixels but the image has {img.pixel_count}")
+    if u.c != v.c:
+        raise DimensionMismatchError(f"membership has {u.c} clusters but centers have {v.c}")
+    out = ctypes.c_double()
+    check(lib().fcm_objective(ptr(img.pixels), ptr(u.u), ptr(v.v), u.n, u.c, m, device, ctypes.byref(out)),
+          None, "objective")
+    return float(out.value)
+
+
+def membership_delta(u_new: MembershipMatrix, u_old: MembershipMatrix, device: int = 0) -> float:
+    """max |u_new - u_old| on the GPU (core.membership_delta, core.py:85-91)."""
+    if (u_new.n, u_new.c) != (u_old.n, u_old.c):
+        raise DimensionMismatchError(f"memberships are {u_new.n}x{u_new.c} and {u_old.n}x{u_old.c}")
+    out = ctypes.c_double()
+    check(lib().fcm_max_abs_diff(ptr(u_new.u), ptr(u_old.u), u_new.n * u_new.c, device, ctypes.byref(out)),
+          None, "max_abs_diff")
+    return float(out.value)
+
+
+def defuzzify(u: MembershipMatrix, width: int, height: int, device: int = 0) -> LabelMap:
+    """Argmax per row, ties to the lowest index (core.defuzzify, core.py:94-102)."""
+    if u.n != width * height:
+        raise DimensionMismatchError(f"membership covers {u.n} pixels but the map is {width}x{height}")
+    labels = np.empty(u.n, dtype=np.int32)
+    check(lib().fcm_argmax_rows(ptr(u.u), ptr(labels), u.n, u.c, device), None, "argmax_rows")
+    return LabelMap(width, height, labels, u.c)

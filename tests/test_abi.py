@@ -1,0 +1,76 @@
+"""The C-ABI library: loads without a GPU, exports every declared symbol,
+validates arguments before touching CUDA (no compute calls here)."""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import REPO
+
+import paper_1601_00072_b200 as pkg
+from paper_1601_00072_b200 import _lib
+
+
+def header_symbols():
+    text = open(os.path.join(REPO, "include", "fcm_b200.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(fcm_\w+)\s*\(", text, re.M)))
+
+
+def test_library_exports_every_header_symbol():
+    L = _lib.lib()
+    syms = header_symbols()
+    assert len(syms) >= 25
+    for s in syms:
+        assert hasattr(L, s), s
+        assert s in _lib.SIGNATURES, f"{s} has no ctypes signature"
+
+
+def test_abi_version_and_status_strings():
+    L = _lib.lib()
+    assert L.fcm_abi_version() == 1
+    assert L.fcm_status_string(_lib.FCM_E_DEGENERATE) == b"degenerate cluster"
+    assert L.fcm_status_string(99) == b"unknown status"
+
+
+def test_argument_validation_is_host_side():
+    L = _lib.lib()
+    h = ctypes.c_void_p()
+    # c < 2, n < c, bad kind, bad shard count: rejected before any CUDA call
+    assert L.fcm_plan_create(ctypes.byref(h), 10, 1, 0, 1, None) == _lib.FCM_E_ARG
+    assert L.fcm_plan_create(ctypes.byref(h), 2, 3, 0, 1, None) == _lib.FCM_E_ARG
+    assert L.fcm_plan_create(ctypes.byref(h), 100, 3, 7, 1, None) == _lib.FCM_E_ARG
+    assert L.fcm_plan_create(ctypes.byref(h), 100, 3, 0, 3, None) == _lib.FCM_E_ARG
+    assert L.fcm_plan_create(ctypes.byref(h), 100, 17, 0, 1, None) == _lib.FCM_E_ARG
+    assert L.fcm_plan_create_rank(ctypes.byref(h), 100, 3, 0, 0, 2, 2, None) == _lib.FCM_E_ARG
+    assert L.fcm_set_option(None, 1, 8) == _lib.FCM_E_ARG
+    assert L.fcm_max_abs_diff(None, None, 4, 0, None) == _lib.FCM_E_ARG
+
+
+def test_no_gpu_means_loud_failure_not_fallback():
+    cnt = ctypes.c_int32(-1)
+    st = _lib.lib().fcm_device_count(ctypes.byref(cnt))
+    if st == _lib.FCM_OK and cnt.value > 0:
+        pytest.skip("a GPU is present")
+    with pytest.raises(pkg.DeviceError):
+        pkg.run_fcm_gpu(pkg.GrayImage(4, 1, [1.0, 2.0, 3.0, 4.0]), pkg.FcmConfig(c=2))
+
+
+def test_pixel_kind_selection():
+    k, a = pkg.pixel_kind(np.array([0.0, 17.0, 255.0]))
+    assert k == _lib.FCM_X_U8 and a.dtype == np.uint8
+    k, a = pkg.pixel_kind(np.array([0.0, 256.0]))
+    assert k == _lib.FCM_X_F64
+    k, a = pkg.pixel_kind(np.array([0.5, 2.0]))
+    assert k == _lib.FCM_X_F64
+
+
+def test_product_path_does_not_import_oracle():
+    import sys
+    import subprocess
+    code = ("import sys; sys.path.insert(0, %r); import paper_1601_00072_b200 as p; "
+            "import paper_1601_00072_b200.engine; "
+            "bad=[m for m in sys.modules if m.startswith('oracle')]; assert not bad, bad") % REPO
+    subprocess.run([sys.executable, "-c", code], check=True)

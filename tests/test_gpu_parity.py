@@ -1,0 +1,143 @@
+"""GPU parity: the CUDA path vs the reference (golden fixtures) and the oracle.
+
+Bars (BASELINE.json north_star, and the reference's own engine-vs-engine
+pins, test_parallel.py:203-212):
+* same iteration count and converged flag,
+* centers within rtol 1e-9 (north star: 1e-4),
+* memberships within 1e-6 absolute (north star: 1e-5),
+* identical hard labels, objective trace within rtol 1e-9.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import golden, mixture_pixels, run_case, run_cases
+
+import paper_1601_00072_b200 as pkg
+
+pytestmark = pytest.mark.gpu
+
+CENTER_RTOL = 1e-9
+U_ATOL = 1e-6
+TRACE_RTOL = 1e-9
+
+
+def _gpu_run(x, c, m, eps, max_iters, seed, devices=None, width=None, height=1, initial=None):
+    width = width or x.shape[0]
+    img = pkg.GrayImage(width, height if width * height == x.shape[0] else x.shape[0] // width, x)
+    cfg = pkg.FcmConfig(c=c, m=m, epsilon=eps, max_iters=max_iters, seed=seed)
+    return pkg.run_fcm_gpu(img, cfg, devices=devices, initial_membership=initial)
+
+
+def _assert_parity(res, r):
+    assert res.iterations == r["iterations"]
+    assert res.converged == r["converged"]
+    assert np.allclose(res.centers.v, r["v"], rtol=CENTER_RTOL, atol=1e-12)
+    assert np.array_equal(res.labels.labels, r["labels"])
+    assert np.allclose(np.array(res.objective_trace), r["trace"], rtol=TRACE_RTOL, atol=1e-9)
+    if r["u"] is not None:
+        assert np.abs(res.membership.u - r["u"]).max() <= U_ATOL
+
+
+@pytest.mark.parametrize("name", run_cases())
+def test_reference_runs(name):
+    r = run_case(name)
+    res = _gpu_run(r["x"], r["c"], r["m"], r["epsilon"], r["max_iters"], r["seed"])
+    _assert_parity(res, r)
+
+
+@pytest.mark.parametrize("devices", [[0, 0], [0, 0, 0, 0], [0] * 8])
+def test_shard_count_invariance_bitwise(devices):
+    # GPU analogue of worker-count invariance (reference test_parallel.py:214-223)
+    r = run_case("C1")
+    base = _gpu_run(r["x"], 3, 2.0, 1e-5, 500, 0)
+    other = _gpu_run(r["x"], 3, 2.0, 1e-5, 500, 0, devices=devices)
+    assert other.centers.v.tobytes() == base.centers.v.tobytes()
+    assert other.membership.u.tobytes() == base.membership.u.tobytes()
+    assert other.objective_trace == base.objective_trace
+    assert other.iterations == base.iterations
+    assert np.array_equal(other.labels.labels, base.labels.labels)
+
+
+def test_determinism_bitwise():
+    x = mixture_pixels(50_000, 3, seed=14)
+    a = _gpu_run(x, 3, 2.0, 1e-6, 500, 99)
+    b = _gpu_run(x, 3, 2.0, 1e-6, 500, 99)
+    assert a.membership.u.tobytes() == b.membership.u.tobytes()
+    assert a.centers.v.tobytes() == b.centers.v.tobytes()
+    assert a.objective_trace == b.objective_trace
+
+
+def test_explicit_initial_membership_matches_seeded():
+    from oracle import oracle as O
+    r = run_case("phantom_c4")
+    u0 = pkg.MembershipMatrix(r["x"].shape[0], 4, O.fill_membership_random(r["x"].shape[0], 4, r["seed"]))
+    res = _gpu_run(r["x"], 4, 2.0, r["epsilon"], r["max_iters"], 12345, initial=u0)
+    _assert_parity(res, r)
+
+
+def test_float_pixels_path_vs_oracle():
+    # non-integer / >255 intensities keep the fp64 pixel path (types.py:38-41)
+    from oracle import oracle as O
+    for x, c, m in ((mixture_pixels(3000, 3, seed=13) + 40.0, 3, 2.0),
+                    (mixture_pixels(2000, 4, seed=4) * 1.37 + 0.25, 4, 1.5),
+                    (mixture_pixels(1500, 2, seed=6) / 7.0, 2, 3.0)):
+        assert pkg.pixel_kind(x)[0] == 2
+        ref = O.run_fcm(x, c, m, 1e-6, 500, 7)
+        res = _gpu_run(x, c, m, 1e-6, 500, 7)
+        assert res.iterations == ref["iterations"]
+        assert np.allclose(res.centers.v, ref["centers"], rtol=CENTER_RTOL)
+        assert np.abs(res.membership.u - ref["membership"]).max() <= U_ATOL
+        assert np.array_equal(res.labels.labels, ref["labels"])
+
+
+def test_shift_property_at_m2():
+    # reference test_core.py:310-317 on the GPU
+    x = mixture_pixels(300, 3, seed=13)
+    a = _gpu_run(x, 3, 2.0, 0.005, 500, 13)
+    b = _gpu_run(x + 40.0, 3, 2.0, 0.005, 500, 13)
+    assert np.allclose(b.centers.v, a.centers.v + 40.0, rtol=0, atol=1e-6)
+    assert np.array_equal(a.labels.labels, b.labels.labels)
+
+
+def test_permutation_equivariance_three_clusters():
+    # reference test_core.py:282-308
+    x = mixture_pixels(300, 3, seed=12)
+    u0 = pkg.init_membership(300, pkg.FcmConfig(c=3, seed=12))
+    perm = [2, 0, 1]
+    up = pkg.MembershipMatrix(300, 3, u0.as_rows()[:, perm].reshape(-1))
+    a = _gpu_run(x, 3, 2.0, 0.005, 500, 12, initial=u0)
+    b = _gpu_run(x, 3, 2.0, 0.005, 500, 12, initial=up)
+    assert a.iterations == b.iterations
+    assert np.allclose(b.centers.v, a.centers.v[perm], rtol=1e-9)
+    relabel = np.empty(3, dtype=np.int32)
+    for new_j, old_j in enumerate(perm):
+        relabel[old_j] = new_j
+    assert np.array_equal(relabel[a.labels.labels], b.labels.labels)
+
+
+def test_objective_descends_and_rows_sum_to_one():
+    x = mixture_pixels(20_000, 4, seed=29)
+    res = _gpu_run(x, 4, 2.0, 1e-6, 500, 29)
+    tr = res.objective_trace
+    for prev, nxt in zip(tr, tr[1:]):
+        assert nxt <= prev + 1e-7 * (1.0 + prev)
+    rows = res.membership.as_rows().sum(axis=1)
+    assert np.abs(rows - 1.0).max() <= 1e-9
+
+
+def test_degenerate_cluster_raises():
+    img = pkg.GrayImage(2, 1, [1.0, 2.0])
+    with pytest.raises(pkg.DegenerateClusterError) as e:
+        pkg.run_fcm_gpu(img, pkg.FcmConfig(c=2), initial_membership=pkg.MembershipMatrix(2, 2, [1, 0, 1, 0]))
+    assert e.value.cluster == 1
+
+
+def test_iterate_matches_reference_contract():
+    r = run_case("C1")
+    from oracle import oracle as O
+    u0 = O.fill_membership_random(r["x"].shape[0], 3, 0)
+    v, u, k, trace, conv = pkg._iterate(r["x"], u0, pkg.FcmConfig(c=3, m=2.0, epsilon=1e-5))
+    assert k == r["iterations"] and conv == r["converged"] and len(trace) == k
+    assert np.allclose(v, r["v"], rtol=CENTER_RTOL)
+    assert np.abs(u - r["u"]).max() <= U_ATOL
