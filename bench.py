@@ -41,7 +41,9 @@ CONFIGS = {
     "C4": ((512, 512, 512), 3, 2.0, 1e-5),
     "C2": ((181, 217, 181), 3, 2.0, 1e-5),
     "C5": ((512, 1024, 1024), 8, 1.5, 1e-5),
+    "C5s": ((64, 1024, 1024), 8, 1.5, 1e-5),  # 64-slice slab of C5 (profiling)
 }
+KERNELS = {"tma": 0, "ldg": 1, "lut": 2, "direct": 3}
 BYTES_PER_VOXEL_ITER = {3: 25, 8: 65}  # x (u8) + read u_{k-1} fp32 SoA + write u_k
 
 
@@ -85,10 +87,14 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            t0 = time.time()
+            while not self.lines and time.time() - t0 < 3.0:  # first sample before timing starts
+                time.sleep(0.01)
+            self.lines.clear()
         except Exception:
             self.proc = None
         return self
@@ -136,10 +142,15 @@ def make_volume(shape, rank_slice=None):
 
 
 # --------------------------------------------------------------- CPU legs --
-def cpu_reference_sample(shape, c, m, eps, slab=32, iters=3):
-    """Reference CPU engine on a slab of the same volume: voxel-iter/s, kind, cores, sample."""
+def cpu_reference_sample(shape, c, m, eps, slab=None, iters=3):
+    """Reference CPU engine on a slab of the same volume: voxel-iter/s, kind, cores, sample.
+
+    Default slab: ~1e8 * 3/c voxel-iterations (~3-10 s on a 16-core host).
+    """
     from paper_1601_00072_b200.phantom import phantom_slice
     nz, ny, nx = shape
+    if slab is None:
+        slab = int(max(1, min(nz, round(1e8 * 3 / c / iters / (nx * ny)))))
     z0 = nz // 2 - slab // 2
     x = np.stack([phantom_slice(nx, ny, (z - nz / 2) / nz, seed=5 * 100003 + z) for z in range(z0, z0 + slab)])
     x = x.reshape(-1).astype(np.float64)
@@ -192,8 +203,7 @@ def run_ours(args, rank, world, local_rank, dist):
     del x_full
     plan.upload_pixels(x)
     plan.init_membership(0)
-    plan.set_option(_lib.FCM_OPT_TIMING, 1)
-    plan.set_option(_lib.FCM_OPT_KERNEL, 0 if args.kernel == "tma" else 1)
+    plan.set_option(_lib.FCM_OPT_KERNEL, KERNELS[args.kernel])
 
     def barrier():
         if world > 1:
@@ -210,23 +220,34 @@ def run_ours(args, rank, world, local_rank, dist):
     for _ in range(args.warmup):
         plan.run(m, eps, max_iters)
 
-    # ---- device-resident timed region: K solves, CUDA events inside fcm_run
+    # ---- device-resident timed region: K solves.  Each fcm_run is one CUDA
+    # graph (prologue + device-side while loop); CUDA events around it.
     barrier()
-    loop_ms, pass_ms, iters, launched = [], [], [], []
+    loop_ms, iters, launched = [], [], []
     with ClockSampler(local_rank) as clk:
         t_wall = time.perf_counter()
         for _ in range(args.steps):
             v, trace, k, conv = plan.run(m, eps, max_iters)
             t = plan.timing()
             loop_ms.append(t["loop_ms"])
-            pass_ms.append(t["pass_ms"])
             iters.append(k)
             launched.append(int(t["passes_launched"]) + 1)
         t_wall = time.perf_counter() - t_wall
     barrier()
     total_ms = max_over_ranks(sum(loop_ms))
-    pass_avg = max_over_ranks(float(np.mean(pass_ms)))
     info = plan.info()
+
+    # ---- kernel timing: the same solves launched pass by pass with CUDA
+    # events around every pass kernel on the launching stream
+    plan.set_option(_lib.FCM_OPT_TIMING, 1)
+    pass_ms, pro_ms = [], []
+    for _ in range(max(2, min(args.steps, 5))):
+        plan.run(m, eps, max_iters)
+        t = plan.timing()
+        pass_ms.append(t["pass_ms"])
+        pro_ms.append(t["prologue_ms"])
+    plan.set_option(_lib.FCM_OPT_TIMING, 0)
+    pass_avg = max_over_ranks(float(np.mean(pass_ms)))
 
     # ---- e2e: host buffers through the C ABI (upload, solve, download)
     u_host = np.empty(plan.n_local * c, dtype=np.float64)
@@ -293,6 +314,7 @@ def run_ours(args, rank, world, local_rank, dist):
         },
         "hbm_gbs_per_gpu": B * n / world * total_iters / (total_ms / 1e3) / 1e9,
         "pass_ms": pass_avg,
+        "prologue_ms": float(np.mean(pro_ms)),
         "roofline": {
             "bound": "hbm",
             "achieved": achieved,
@@ -302,8 +324,10 @@ def run_ours(args, rank, world, local_rank, dist):
             "traffic": traffic,
             "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured" else peak_kind,
             "bytes_per_voxel_iter": B,
-            "kernel": ("pass_tma_kernel" if args.kernel == "tma" else "pass_kernel")
-            + ("<uint8_t,%d,MODE_M2>" % c if m == 2.0 else "<uint8_t,%d,MODE_GEN>" % c),
+            "kernel": ("pass_kernel" if args.kernel == "ldg" else "pass_tma_kernel")
+            + "<uint8_t,%d,%s>" % (c, "MODE_M2" if m == 2.0 and args.kernel in ("tma", "direct", "ldg")
+                                   else ("MODE_LUT" if args.kernel in ("tma", "lut") else "MODE_GEN")),
+            "timing": "pass kernels timed one by one with CUDA events (FCM_OPT_TIMING) after the graph-launched timed region",
         },
         "e2e": {
             "value": n * e2e_iters / e2e_s,
@@ -330,10 +354,10 @@ def run_reference(args, rank):
     vals = []
     kind = cores = sample = None
     for _ in range(args.warmup):
-        cpu_reference_sample(shape, c, m, eps, slab=8, iters=1)
+        cpu_reference_sample(shape, c, m, eps, slab=4, iters=1)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        v, kind, cores, sample = cpu_reference_sample(shape, c, m, eps, slab=16, iters=2)
+        v, kind, cores, sample = cpu_reference_sample(shape, c, m, eps, slab=max(1, 16 * 3 // c), iters=2)
         vals.append(v)
     dt = time.perf_counter() - t0
     value = float(np.mean(vals))
@@ -361,13 +385,14 @@ def run_reference(args, rank):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C4", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--kernel", default="tma", choices=["tma", "ldg"],
-                    help="pass kernel: TMA bulk-copy pipeline (default) or register-staged LDG/STG")
+    ap.add_argument("--kernel", default="tma", choices=sorted(KERNELS),
+                    help="pass kernel: tma (TMA bulk-copy pipeline, auto math; default), ldg "
+                         "(register-staged LDG/STG), lut (TMA + intensity table), direct (TMA + per-voxel math)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3

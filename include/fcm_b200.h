@@ -53,7 +53,13 @@ typedef enum {
   FCM_OPT_BATCH = 1,   /* passes launched between host checks of the done flag (default 8) */
   FCM_OPT_TIMING = 2,  /* 1: record per-pass CUDA events for fcm_last_timing (default 0) */
   FCM_OPT_GRID = 3,    /* force CTAs per pass launch (0 = occupancy-derived, default) */
-  FCM_OPT_KERNEL = 4   /* pass kernel: 0 = TMA bulk-copy pipeline (default), 1 = register-staged LDG/STG */
+  FCM_OPT_KERNEL = 4,  /* pass kernel: 0 = TMA bulk-copy pipeline, automatic per-voxel math (default:
+                          product form for m == 2, per-pass intensity table for other m on uint8),
+                          1 = register-staged LDG/STG, 2 = TMA + intensity table for every m (uint8),
+                          3 = TMA + per-voxel math for every m */
+  FCM_OPT_GRAPH = 5    /* 1 (default): single-shard runs launch prologue + a device-side while loop
+                          (CUDA graph conditional node) -- no host round trip per iteration;
+                          0: host-driven batches.  FCM_OPT_TIMING forces the host-driven path. */
 } fcm_option;
 
 typedef struct fcm_plan fcm_plan;
@@ -77,7 +83,8 @@ int fcm_plan_create(fcm_plan** out, int64_t n, int32_t c, int32_t x_kind, int32_
 /* One rank of an nranks-process job (one process per GPU): the plan owns the
  * rank's contiguous voxel range (query it with fcm_plan_info) and exchanges
  * the 2c+2 reduction roots with ncclAllGather.  nccl_id is the 128-byte
- * ncclUniqueId from fcm_nccl_unique_id on rank 0 (ignored when nranks == 1). */
+ * ncclUniqueId from fcm_nccl_unique_id on rank 0; NULL is allowed when nranks == 1
+ * (a one-rank id still routes the roots through NCCL, which tests use). */
 int fcm_plan_create_rank(fcm_plan** out, int64_t n_global, int32_t c, int32_t x_kind,
                          int32_t device, int32_t nranks, int32_t rank, const void* nccl_id);
 int fcm_nccl_unique_id(void* out128);

@@ -103,7 +103,19 @@ struct fcm_plan {
   int batch = 8;
   int timing = 0;
   int force_grid = 0;
-  int variant = 0;  // pass kernel: 0 TMA pipeline, 1 register-staged LDG
+  int variant = 0;  // pass kernel: 0 TMA pipeline (auto), 1 register-staged LDG, 2 TMA + intensity table
+  // graph mode: prologue + while(!done) { pass; pass } as ONE CUDA graph with a
+  // device-side conditional loop -- no host round trip per iteration
+  int use_graph = 1;
+  bool capturing = false;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  cudaGraphConditionalHandle gcond = 0;
+  struct GraphKey {
+    double m, eps;
+    int max_iters, init_src, variant, force_grid;
+    uint64_t seed;
+  } gkey{};
   Control* host_ctl = nullptr;   // pinned: device -> host reads of the control block
   Control* host_tmpl = nullptr;  // pinned: reset template copied to every shard
   std::vector<cudaEvent_t> ev_t0, ev_t1;
@@ -219,6 +231,7 @@ int setup_shard(fcm_plan* p, Shard& s) {
   return FCM_OK;
 }
 
+void drop_graph(fcm_plan* p);
 void release(fcm_plan* p) {
   for (int i = 0; i < p->nshards; ++i) {
     Shard& s = p->sh[i];
@@ -237,6 +250,7 @@ void release(fcm_plan* p) {
   if (p->ev_end) cudaEventDestroy(p->ev_end);
   if (p->host_ctl) cudaFreeHost(p->host_ctl);
   if (p->host_tmpl) cudaFreeHost(p->host_tmpl);
+  drop_graph(p);
   if (p->comm && g_nccl.ok) g_nccl.CommDestroy(p->comm);
 }
 
@@ -324,6 +338,9 @@ PassArgs make_args(fcm_plan* p, Shard& s, int seq, double eps, int max_iters) {
   a.oct_cnt = s.oct_cnt;
   a.ctl = s.ctl;
   a.trace = s.trace;
+  a.cond = p->gcond;
+  a.use_cond = p->capturing ? 1 : 0;
+  a.finalize_local = (p->nranks == 1 && !p->use_nccl) ? 1 : 0;
   return a;
 }
 
@@ -339,7 +356,7 @@ int step(fcm_plan* p, int seq, double eps, int max_iters) {
     if (s.g.tiles_local == 0) {
       CK(cudaMemsetAsync(a.rank_root, 0, sizeof(double) * nf, s.stream));
     } else if (prologue) {
-      CK(launch_prologue(p->xkind, p->c, p->init_src == 1, a, s.sms, s.stream));
+      CK(launch_prologue(p->xkind, p->c, p->mode, p->init_src == 1, a, s.sms, s.stream));
     } else {
       int grid = 0;
       const bool t = p->timing && i == 0;
@@ -361,7 +378,7 @@ int step(fcm_plan* p, int seq, double eps, int max_iters) {
     }
   }
   if (!prologue) p->passes_launched++;
-  if (p->nranks == 1) return FCM_OK;
+  if (p->nranks == 1 && !p->use_nccl) return FCM_OK;
 
   FinalizeArgs f{};
   f.nranks = p->nranks;
@@ -369,6 +386,8 @@ int step(fcm_plan* p, int seq, double eps, int max_iters) {
   f.eps = eps;
   f.max_iters = max_iters;
   f.prologue = prologue ? 1 : 0;
+  f.cond = p->gcond;
+  f.use_cond = p->capturing ? 1 : 0;
   if (p->use_nccl) {
     Shard& s = p->sh[0];
     ncclResult_t r = g_nccl.AllGather(s.rank_root + (seq & 1) * nf, s.gathered, (size_t)nf,
@@ -399,6 +418,71 @@ int step(fcm_plan* p, int seq, double eps, int max_iters) {
 }
 
 int check_plan(fcm_plan* p) { return p ? FCM_OK : FCM_E_ARG; }
+
+void drop_graph(fcm_plan* p) {
+  if (p->gexec) cudaGraphExecDestroy(p->gexec);
+  if (p->graph) cudaGraphDestroy(p->graph);
+  p->gexec = nullptr;
+  p->graph = nullptr;
+}
+
+// prologue -> while (cond) { pass(odd); pass(even) } on shard 0's stream.
+// The conditional handle defaults to 1 at every launch; whichever kernel
+// observes `done` (finalize, or an early-exiting pass) sets it to 0.
+int build_graph(fcm_plan* p, double eps, int max_iters) {
+  drop_graph(p);
+  Shard& s = p->sh[0];
+  CK(cudaSetDevice(s.device));
+  CK(cudaGraphCreate(&p->graph, 0));
+  CK(cudaGraphConditionalHandleCreate(&p->gcond, p->graph, 1u, cudaGraphCondAssignDefault));
+  p->capturing = true;
+  int rc = FCM_OK;
+  cudaGraph_t g_out = nullptr;
+  if (cudaStreamBeginCaptureToGraph(s.stream, p->graph, nullptr, nullptr, 0,
+                                    cudaStreamCaptureModeRelaxed) != cudaSuccess) {
+    p->capturing = false;
+    return fail(p, FCM_E_CUDA, "cudaStreamBeginCaptureToGraph failed");
+  }
+  rc = step(p, 0, eps, max_iters);
+  cudaError_t ec = cudaStreamEndCapture(s.stream, &g_out);
+  if (rc || ec != cudaSuccess) {
+    p->capturing = false;
+    drop_graph(p);
+    return rc ? rc : fail(p, FCM_E_CUDA, "prologue capture: %s", cudaGetErrorString(ec));
+  }
+  size_t nn = 0;
+  CK(cudaGraphGetNodes(p->graph, nullptr, &nn));
+  std::vector<cudaGraphNode_t> deps(nn);
+  CK(cudaGraphGetNodes(p->graph, deps.data(), &nn));
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = p->gcond;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t cnode;
+  CK(cudaGraphAddNode(&cnode, p->graph, deps.data(), nn, &cp));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  if (cudaStreamBeginCaptureToGraph(s.stream, body, nullptr, nullptr, 0,
+                                    cudaStreamCaptureModeRelaxed) != cudaSuccess) {
+    p->capturing = false;
+    drop_graph(p);
+    return fail(p, FCM_E_CUDA, "body capture failed");
+  }
+  rc = step(p, 1, eps, max_iters);
+  if (!rc) rc = step(p, 2, eps, max_iters);
+  ec = cudaStreamEndCapture(s.stream, &g_out);
+  p->capturing = false;
+  if (rc || ec != cudaSuccess) {
+    drop_graph(p);
+    return rc ? rc : fail(p, FCM_E_CUDA, "body capture: %s", cudaGetErrorString(ec));
+  }
+  ec = cudaGraphInstantiate(&p->gexec, p->graph, 0);
+  if (ec != cudaSuccess) {
+    drop_graph(p);
+    return fail(p, FCM_E_CUDA, "cudaGraphInstantiate: %s", cudaGetErrorString(ec));
+  }
+  return FCM_OK;
+}
 }  // namespace
 
 // ================================================================== C ABI ==
@@ -509,7 +593,9 @@ int fcm_plan_create_rank(fcm_plan** out, int64_t n_global, int32_t c, int32_t x_
   base_geometry(n_global, p->sh[0].g);
   rank_geometry(p->sh[0].g, nranks, rank);
   int rc = common_setup(p);
-  if (!rc && nranks > 1) {
+  // nranks == 1 with an id still builds a (one-rank) communicator: the NCCL
+  // exchange path then runs end to end on a single GPU (tests).
+  if (!rc && (nranks > 1 || nccl_id)) {
     if (!nccl_id || !load_nccl()) {
       rc = fail(p, FCM_E_NCCL, "NCCL unavailable (set FCM_NCCL_LIB) or no unique id");
     } else {
@@ -552,8 +638,9 @@ int fcm_set_option(fcm_plan* p, int32_t key, int64_t value) {
       if (value < 0) return FCM_E_ARG;
       p->force_grid = (int)value;
       return FCM_OK;
+    case FCM_OPT_GRAPH: p->use_graph = value ? 1 : 0; return FCM_OK;
     case FCM_OPT_KERNEL:
-      if (value != 0 && value != 1) return FCM_E_ARG;
+      if (value < 0 || value > 3) return FCM_E_ARG;
       p->variant = (int)value;
       return FCM_OK;
     default: return FCM_E_ARG;
@@ -654,20 +741,41 @@ int fcm_run(fcm_plan* p, double m, double eps, int32_t max_iters, double* v_out,
   Shard& s0 = p->sh[0];
   CK(cudaSetDevice(s0.device));
   p->passes_launched = 0;
-  CK(cudaEventRecord(p->ev_start, s0.stream));
-  int rc = step(p, 0, eps, max_iters);
-  if (rc) return rc;
-  CK(cudaSetDevice(s0.device));
-  CK(cudaEventRecord(p->ev_pro, s0.stream));
-  int seq = 1;
-  while (seq <= max_iters) {
-    const int nb = std::min(p->batch, max_iters - seq + 1);
-    for (int b = 0; b < nb; ++b, ++seq)
-      if ((rc = step(p, seq, eps, max_iters))) return rc;
+  int rc = FCM_OK;
+  const bool graph = p->use_graph && p->nshards == 1 && !p->timing;
+  if (graph) {
+    fcm_plan::GraphKey key;
+    memset(&key, 0, sizeof key);  // padding takes part in the memcmp below
+    key.m = m;
+    key.eps = eps;
+    key.max_iters = max_iters;
+    key.init_src = p->init_src;
+    key.variant = p->variant;
+    key.force_grid = p->force_grid;
+    key.seed = p->seed;
+    if (!p->gexec || memcmp(&key, &p->gkey, sizeof key) != 0) {
+      if ((rc = build_graph(p, eps, max_iters))) return rc;
+      p->gkey = key;
+    }
+    CK(cudaEventRecord(p->ev_start, s0.stream));
+    CK(cudaGraphLaunch(p->gexec, s0.stream));
+    CK(cudaEventRecord(p->ev_pro, s0.stream));
+  } else {
+    CK(cudaEventRecord(p->ev_start, s0.stream));
+    rc = step(p, 0, eps, max_iters);
+    if (rc) return rc;
     CK(cudaSetDevice(s0.device));
-    CK(cudaMemcpyAsync(p->host_ctl, s0.ctl, sizeof(Control), cudaMemcpyDeviceToHost, s0.stream));
-    CK(cudaStreamSynchronize(s0.stream));
-    if (p->host_ctl->done) break;
+    CK(cudaEventRecord(p->ev_pro, s0.stream));
+    int seq = 1;
+    while (seq <= max_iters) {
+      const int nb = std::min(p->batch, max_iters - seq + 1);
+      for (int b = 0; b < nb; ++b, ++seq)
+        if ((rc = step(p, seq, eps, max_iters))) return rc;
+      CK(cudaSetDevice(s0.device));
+      CK(cudaMemcpyAsync(p->host_ctl, s0.ctl, sizeof(Control), cudaMemcpyDeviceToHost, s0.stream));
+      CK(cudaStreamSynchronize(s0.stream));
+      if (p->host_ctl->done) break;
+    }
   }
   CK(cudaSetDevice(s0.device));
   CK(cudaEventRecord(p->ev_end, s0.stream));
@@ -684,6 +792,7 @@ int fcm_run(fcm_plan* p, double m, double eps, int32_t max_iters, double* v_out,
   CK(cudaEventElapsedTime(&ms, p->ev_start, p->ev_pro));
   p->t_pro_ms = ms;
   p->passes_done = h.iter;
+  if (graph) p->passes_launched = (int)h.launches;
   p->t_pass_ms = 0;
   if (p->timing && h.iter > 0) {
     double tot = 0;
@@ -700,6 +809,7 @@ int fcm_run(fcm_plan* p, double m, double eps, int32_t max_iters, double* v_out,
   if (trace_out && h.iter > 0)
     CK(cudaMemcpy(trace_out, s0.trace, sizeof(double) * h.iter, cudaMemcpyDeviceToHost));
   if (!h.done) return fail(p, FCM_E_STATE, "loop ended without the done flag");
+  if (h.dead == -2) return fail(p, FCM_E_STATE, "device loop watchdog fired (internal error)");
   if (h.dead >= 0) return fail(p, FCM_E_DEGENERATE, "cluster %d has zero total membership weight", h.dead);
   p->run_ok = true;
   return FCM_OK;

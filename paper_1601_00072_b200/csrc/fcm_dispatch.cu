@@ -7,7 +7,7 @@ namespace fcm {
 
 #define FCM_EXTERN(C)                                                                                \
   extern template cudaError_t launch_pass_c<C>(int, int, const PassArgs&, int, cudaStream_t, int*, int, int); \
-  extern template cudaError_t launch_prologue_c<C>(int, bool, const PassArgs&, int, cudaStream_t);  \
+  extern template cudaError_t launch_prologue_c<C>(int, int, bool, const PassArgs&, int, cudaStream_t); \
   extern template cudaError_t launch_epilogue_c<C>(int, int, const EpilogueArgs&, int, cudaStream_t);
 FCM_EXTERN(2) FCM_EXTERN(3) FCM_EXTERN(4) FCM_EXTERN(5) FCM_EXTERN(6) FCM_EXTERN(7) FCM_EXTERN(8) FCM_EXTERN(16)
 
@@ -17,14 +17,18 @@ __global__ void finalize_kernel(FinalizeArgs a) {
   __shared__ double root[kNFMax];
   const int nf = 2 * a.c + 2;
   const int lane = threadIdx.x;
-  if (*(volatile int*)&a.ctl->done) return;
+  if (*(volatile int*)&a.ctl->done) {
+    if (a.use_cond && lane == 0) cudaGraphSetConditional(a.cond, 0u);
+    return;
+  }
   for (int f = 0; f < nf; ++f) {
     double v = lane < a.nranks ? __ldcg(&a.roots[lane][f]) : 0.0;
     v = warp_tree(v, f == nf - 1);
     if (lane == 0) root[f] = v;
   }
   __syncwarp();
-  if (lane == 0) finalize(a.ctl, root, a.c, a.eps, a.max_iters, a.trace, a.prologue != 0);
+  if (lane == 0)
+    finalize(a.ctl, root, a.c, a.eps, a.max_iters, a.trace, a.prologue != 0, a.cond, a.use_cond);
 }
 
 
@@ -49,10 +53,10 @@ cudaError_t launch_pass(int xkind, int c, int mode, const PassArgs& a, int sms, 
 #undef CALL
 }
 
-cudaError_t launch_prologue(int xkind, int c, bool from_seed, const PassArgs& a, int sms,
+cudaError_t launch_prologue(int xkind, int c, int mode, bool from_seed, const PassArgs& a, int sms,
                             cudaStream_t st) {
   if (c < 2 || c > kCMaxSupported) return cudaErrorInvalidValue;
-#define CALL(C) launch_prologue_c<C>(xkind, from_seed, a, sms, st)
+#define CALL(C) launch_prologue_c<C>(xkind, mode, from_seed, a, sms, st)
   FCM_SWITCH(CALL)
 #undef CALL
 }

@@ -21,7 +21,7 @@ namespace fcm {
 
 template <int NF>
 struct SmemRedT {
-  double w[kWarps][NF];
+  double w[2][kWarps][NF];
   double root[NF];
   int tile;
   int flag;
@@ -48,8 +48,8 @@ __device__ __forceinline__ int field_of(int s, int c) {
 // ----------------------------------------------------------- finalize -----
 // Consumes the global root of pass k (or of the prologue) and prepares the
 // centers of the next pass; mirrors the control flow of core._iterate.
-__device__ inline void finalize(Control* ctl, const double* root, int c, double eps, int max_iters,
-                         double* trace, bool prologue) {
+__device__ inline void finalize_body(Control* ctl, const double* root, int c, double eps, int max_iters,
+                                     double* trace, bool prologue) {
   const int nf = 2 * c + 2;
   for (int f = 0; f < nf; ++f) ctl->root[f] = root[f];
   if (!prologue) {
@@ -77,14 +77,57 @@ __device__ inline void finalize(Control* ctl, const double* root, int c, double 
   for (int j = 0; j < c; ++j) ctl->v[j] = root[j] / root[c + j];
 }
 
+// finalize + stop the device-side while loop (graph mode) once done.
+__device__ inline void finalize(Control* ctl, const double* root, int c, double eps, int max_iters,
+                                double* trace, bool prologue, cudaGraphConditionalHandle cond,
+                                int use_cond) {
+  finalize_body(ctl, root, c, eps, max_iters, trace, prologue);
+  if (use_cond && ctl->done) cudaGraphSetConditional(cond, 0u);
+}
+
+// Uniform early exit of a pass launched after the loop finished; CTA 0 also
+// closes the device-side loop so a graph never spins on finished work.
+template <typename SM>
+__device__ __forceinline__ bool pass_done(const PassArgs& a, SM& sm) {
+  if (threadIdx.x == 0) {
+    int done = *(volatile int*)&a.ctl->done;
+    if (blockIdx.x == 0 && a.seq != 0) {
+      const unsigned launched = a.ctl->launches++;
+      if (!done && a.use_cond && launched > (unsigned)a.max_iters + 8u) {
+        // watchdog: a device loop may never outlive max_iters passes
+        a.ctl->dead = -2;
+        a.ctl->done = 1;
+        done = 1;
+      }
+      if (done && a.use_cond) cudaGraphSetConditional(a.cond, 0u);
+    }
+    sm.flag = done;
+  }
+  __syncthreads();
+  return sm.flag != 0;
+}
+
 // ----------------------------------------------------------- tile tree ----
+// acq_rel device-scope counter increment: publishes this thread's stores (and
+// everything it observed) and, for the last arriver, makes the other
+// arrivals' stores visible.  Replaces a full __threadfence on every thread.
+__device__ __forceinline__ unsigned atom_add_acq_rel(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
 // Reduce the per-thread payload of local tile lt to the tile partial, then
 // climb the tree: the CTA that completes a group of 32 tiles reduces the
 // group, the one that completes an octant reduces the octant, the one that
 // completes the rank reduces the rank (and finalizes when it is alone).
+// Only warp 0 goes past the first barrier, so the other warps return to the
+// stream at once; `buf` double-buffers the per-warp scratch for that reason.
+// Lane 0 writes every tree node it publishes, so its acq_rel counter update
+// orders exactly the stores it covers.
 template <int C, bool NAMED = false, typename SM>
 __device__ __forceinline__ void tile_finish(const PassArgs& a, int lt, const double* acc, SM& sm,
-                            bool prologue) {
+                                            bool prologue, int buf = 0) {
   constexpr int NS = 2 * C + 2;
   const int c = C <= 8 ? C : a.c, nf = 2 * c + 2;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -94,33 +137,39 @@ __device__ __forceinline__ void tile_finish(const PassArgs& a, int lt, const dou
   for (int s = 0; s < NS; ++s) {
     double r = warp_tree(acc[s], s == NS - 1);
     int f = field_of<C>(s, c);
-    if (lane == 0 && f >= 0) sm.w[warp][f] = r;
+    if (lane == 0 && f >= 0) sm.w[buf][warp][f] = r;
   }
   red_sync<NAMED>();
-  if (tid < nf) {
-    const bool mx = tid == nf - 1;
-    double q0 = combine(sm.w[0][tid], sm.w[1][tid], mx), q1 = combine(sm.w[2][tid], sm.w[3][tid], mx);
-    double q2 = combine(sm.w[4][tid], sm.w[5][tid], mx), q3 = combine(sm.w[6][tid], sm.w[7][tid], mx);
-    a.tile_part[(int64_t)lt * nf + tid] = combine(combine(q0, q1, mx), combine(q2, q3, mx), mx);
+  if (warp != 0) return;
+
+  // tile partial: adjacent-pair tree over the 8 warps, field per lane
+  double part = 0.0;
+  if (lane < nf) {
+    const bool mx = lane == nf - 1;
+    const double q0 = combine(sm.w[buf][0][lane], sm.w[buf][1][lane], mx);
+    const double q1 = combine(sm.w[buf][2][lane], sm.w[buf][3][lane], mx);
+    const double q2 = combine(sm.w[buf][4][lane], sm.w[buf][5][lane], mx);
+    const double q3 = combine(sm.w[buf][6][lane], sm.w[buf][7][lane], mx);
+    part = combine(combine(q0, q1, mx), combine(q2, q3, mx), mx);
   }
-  __threadfence();
-  red_sync<NAMED>();
+  for (int f = 0; f < nf; ++f) {
+    const double v = __shfl_sync(0xffffffffu, part, f);
+    if (lane == 0) a.tile_part[(int64_t)lt * nf + f] = v;
+  }
 
   const int gt = g.tile0 + lt;
   const int oct = gt / g.M;
   const int grp = (gt - oct * g.M) / kGroup;
   const int loct = oct - g.oct0;
   const int lgrp = loct * g.gpo + grp;
-  if (tid == 0) {
-    unsigned prev = atomicAdd(&a.group_cnt[lgrp], 1u);
-    sm.flag = (int)prev == group_real_tiles(g, oct, grp) - 1;
-  }
-  red_sync<NAMED>();
-  if (!sm.flag) return;
+  unsigned prev = 0;
+  if (lane == 0) prev = atom_add_acq_rel(&a.group_cnt[lgrp], 1u);
+  prev = __shfl_sync(0xffffffffu, prev, 0);
+  if ((int)prev != group_real_tiles(g, oct, grp) - 1) return;
 
-  if (warp == 0) {
-    if (lane == 0) a.group_cnt[lgrp] = 0u;
-    __threadfence();
+  // last tile of the group: reduce the group's 32 leaves
+  if (lane == 0) a.group_cnt[lgrp] = 0u;
+  {
     const int leaf = grp * kGroup + lane;
     const bool real = leaf < g.M && (int64_t)oct * g.M + leaf < g.T;
     const int64_t lt_leaf = (int64_t)oct * g.M + leaf - g.tile0;
@@ -130,18 +179,13 @@ __device__ __forceinline__ void tile_finish(const PassArgs& a, int lt, const dou
       if (lane == 0) a.group_root[(int64_t)lgrp * nf + f] = v;
     }
   }
-  __threadfence();
-  red_sync<NAMED>();
-  if (tid == 0) {
-    unsigned prev = atomicAdd(&a.oct_cnt[loct], 1u);
-    sm.flag = (int)prev == octant_real_groups(g, oct) - 1;
-  }
-  red_sync<NAMED>();
-  if (!sm.flag) return;
+  if (lane == 0) prev = atom_add_acq_rel(&a.oct_cnt[loct], 1u);
+  prev = __shfl_sync(0xffffffffu, prev, 0);
+  if ((int)prev != octant_real_groups(g, oct) - 1) return;
 
-  if (warp == 0) {
-    if (lane == 0) a.oct_cnt[loct] = 0u;
-    __threadfence();
+  // last group of the octant
+  if (lane == 0) a.oct_cnt[loct] = 0u;
+  {
     const bool real = lane < g.gpo && group_real_tiles(g, oct, lane) > 0;
     for (int f = 0; f < nf; ++f) {
       double v = real ? __ldcg(&a.group_root[((int64_t)loct * g.gpo + lane) * nf + f]) : 0.0;
@@ -149,18 +193,13 @@ __device__ __forceinline__ void tile_finish(const PassArgs& a, int lt, const dou
       if (lane == 0) a.oct_root[loct * nf + f] = v;
     }
   }
-  __threadfence();
-  red_sync<NAMED>();
-  if (tid == 0) {
-    unsigned prev = atomicAdd(&a.ctl->rank_cnt, 1u);
-    sm.flag = (int)prev == rank_real_octants(g) - 1;
-  }
-  red_sync<NAMED>();
-  if (!sm.flag) return;
+  if (lane == 0) prev = atom_add_acq_rel(&a.ctl->rank_cnt, 1u);
+  prev = __shfl_sync(0xffffffffu, prev, 0);
+  if ((int)prev != rank_real_octants(g) - 1) return;
 
-  if (warp == 0) {
-    if (lane == 0) a.ctl->rank_cnt = 0u;
-    __threadfence();
+  // last octant of the rank: the rank root (and, alone, the finalize)
+  if (lane == 0) a.ctl->rank_cnt = 0u;
+  {
     const bool real = lane < g.noct && (int64_t)(g.oct0 + lane) * g.M < g.T;
     for (int f = 0; f < nf; ++f) {
       double v = real ? __ldcg(&a.oct_root[lane * nf + f]) : 0.0;
@@ -170,8 +209,10 @@ __device__ __forceinline__ void tile_finish(const PassArgs& a, int lt, const dou
         sm.root[f] = v;
       }
     }
-    if (lane == 0 && g.nranks == 1)
-      finalize(a.ctl, sm.root, c, a.eps, a.max_iters, a.trace, prologue);
+  }
+  __syncwarp();
+  if (lane == 0) {
+    if (a.finalize_local) finalize(a.ctl, sm.root, c, a.eps, a.max_iters, a.trace, prologue, a.cond, a.use_cond);
     __threadfence();
   }
 }
@@ -274,9 +315,7 @@ __device__ __forceinline__ void pass_tile(const PassArgs& a, int lt, const doubl
 template <typename XT, int C, int MODE>
 __global__ void __launch_bounds__(kThreads) pass_kernel(PassArgs a) {
   __shared__ SmemRed sm;
-  if (threadIdx.x == 0) sm.flag = *(volatile int*)&a.ctl->done;
-  __syncthreads();
-  if (sm.flag) return;
+  if (pass_done(a, sm)) return;
   if (blockIdx.x == 0 && threadIdx.x == 0) a.ctl->tile_next[(a.seq + 1) & 1] = 0u;
   double v[C];
 #pragma unroll
@@ -305,15 +344,15 @@ __global__ void __launch_bounds__(kThreads) pass_kernel(PassArgs a) {
 // give v_1, from either the seeded generator (bit-exact with
 // core.init_membership) or an uploaded fp64 AoS initial membership.
 template <typename XT, int C, int MODE, bool FROM_SEED>
-__global__ void __launch_bounds__(kThreads) prologue_kernel(PassArgs a) {
-  __shared__ SmemRed sm;
-  if (threadIdx.x == 0) sm.flag = *(volatile int*)&a.ctl->done;
-  __syncthreads();
-  if (sm.flag) return;
+__global__ void __launch_bounds__(kThreads, 2) prologue_kernel(PassArgs a) {
+  __shared__ SmemRedT<2 * C + 2> sm;
+  if (pass_done(a, sm)) return;
   if (blockIdx.x == 0 && threadIdx.x == 0) a.ctl->tile_next[(a.seq + 1) & 1] = 0u;
   const Powers pw = load_powers(a);
-  const int c = a.c;
+  const int c = C <= 8 ? C : a.c;
+  const uint64_t row_step = (uint64_t)c * kGamma;  // SplitMix64 state advance per voxel
   const int ntiles = a.g.tiles_local;
+  const XT* __restrict__ x = reinterpret_cast<const XT*>(a.x);
   for (;;) {
     if (threadIdx.x == 0) sm.tile = (int)atomicAdd(&a.ctl->tile_next[a.seq & 1], 1u);
     __syncthreads();
@@ -324,39 +363,29 @@ __global__ void __launch_bounds__(kThreads) prologue_kernel(PassArgs a) {
 #pragma unroll
     for (int s = 0; s < 2 * C + 2; ++s) acc[s] = 0.0;
     const int64_t base = (int64_t)lt << a.g.tile_shift;
-    const int steps = (1 << a.g.tile_shift) / (kThreads * kVec);
+    const int steps = (1 << a.g.tile_shift) / kThreads;
+    // one voxel per thread per step: consecutive threads -> consecutive
+    // voxels, so every plane store is a coalesced 128-byte warp write
     for (int r = 0; r < steps; ++r) {
-      const int64_t i0 = base + ((int64_t)r * kThreads + threadIdx.x) * kVec;
-      if (i0 >= a.g.n_local) break;
-      double xd[4];
-      XLoad<XT>::load4(reinterpret_cast<const XT*>(a.x), i0, xd);
-      float4 un[C];
+      const int64_t i = base + (int64_t)r * kThreads + threadIdx.x;
+      if (i >= a.g.n_local) break;
+      const double xd = (double)x[i];
+      double u[C];
+      if (FROM_SEED) {
+        init_row_state<C>(a.seed + (uint64_t)(a.g.voxel0 + i) * row_step, c, u);
+      } else {
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int64_t i = i0 + q;
-        const bool valid = i < a.g.n_local;
-        double u[C];
-        if (FROM_SEED) {
-          init_row<C>(a.seed, a.g.voxel0 + i, c, u);
-        } else {
-#pragma unroll
-          for (int j = 0; j < C; ++j) u[j] = (j < c && valid) ? a.u0_aos[i * c + j] : 0.0;
-        }
-#pragma unroll
-        for (int j = 0; j < C; ++j) {
-          if (j < c) {
-            if (valid) {
-              const double w = pow(u[j], a.m);  // exactly the reference's pow(u, m)
-              acc[j] = fma(w, xd[q], acc[j]);
-              acc[C + j] += w;
-            }
-            f4set(un[j], q, (float)u[j]);
-          }
-        }
+        for (int j = 0; j < C; ++j) u[j] = j < c ? a.u0_aos[i * c + j] : 0.0;
       }
 #pragma unroll
-      for (int j = 0; j < C; ++j)
-        if (j < c) *reinterpret_cast<float4*>(a.u_nxt + j * a.g.plane + i0) = un[j];
+      for (int j = 0; j < C; ++j) {
+        if (j < c) {
+          const double w = pow_m<MODE>(u[j], pw);  // the reference's pow(u, m)
+          acc[j] = fma(w, xd, acc[j]);
+          acc[C + j] += w;
+          __stcg(a.u_nxt + j * a.g.plane + i, (float)u[j]);
+        }
+      }
     }
     tile_finish<C>(a, lt, acc, sm, true);
     __syncthreads();
@@ -419,10 +448,15 @@ cudaError_t launch_pass_c(int xkind, int mode, const PassArgs& a, int sms, cudaS
                           int* grid_out, int variant, int force_grid) {
   constexpr int MD = C <= 8 ? MODE_M2 : MODE_GEN;
   const bool m2 = (mode == MODE_M2) && C <= 8;
-  if (variant == 0) {  // TMA bulk pipeline (production)
-    if (xkind == XK_U8)
+  if (variant == 0 || variant == 2 || variant == 3) {  // TMA bulk pipeline (production)
+    if (xkind == XK_U8) {
+      // uint8 pixels: m == 2 -> fused product form; any other m (or variant 2)
+      // -> per-pass intensity table (C <= 8); variant 3 -> direct math always.
+      if (C <= 8 && variant != 3 && (variant == 2 || !m2))
+        return launch_pass_tma<uint8_t, C, (C <= 8 ? MODE_LUT : MODE_GEN)>(a, sms, st, grid_out, force_grid);
       return m2 ? launch_pass_tma<uint8_t, C, MD>(a, sms, st, grid_out, force_grid)
                 : launch_pass_tma<uint8_t, C, MODE_GEN>(a, sms, st, grid_out, force_grid);
+    }
     return m2 ? launch_pass_tma<double, C, MD>(a, sms, st, grid_out, force_grid)
               : launch_pass_tma<double, C, MODE_GEN>(a, sms, st, grid_out, force_grid);
   }
@@ -443,14 +477,17 @@ cudaError_t launch_pass_c(int xkind, int mode, const PassArgs& a, int sms, cudaS
 }
 
 template <int C>
-cudaError_t launch_prologue_c(int xkind, bool from_seed, const PassArgs& a, int sms, cudaStream_t st) {
+cudaError_t launch_prologue_c(int xkind, int mode, bool from_seed, const PassArgs& a, int sms,
+                              cudaStream_t st) {
   auto go = [&](auto k) { k<<<occupancy_grid(k, a.g.tiles_local, sms), kThreads, 0, st>>>(a); };
+  constexpr int MD = C <= 8 ? MODE_M2 : MODE_GEN;
+  const bool m2 = mode == MODE_M2 && C <= 8;
   if (xkind == XK_U8) {
-    if (from_seed) go(prologue_kernel<uint8_t, C, MODE_GEN, true>);
-    else go(prologue_kernel<uint8_t, C, MODE_GEN, false>);
+    if (from_seed) m2 ? go(prologue_kernel<uint8_t, C, MD, true>) : go(prologue_kernel<uint8_t, C, MODE_GEN, true>);
+    else m2 ? go(prologue_kernel<uint8_t, C, MD, false>) : go(prologue_kernel<uint8_t, C, MODE_GEN, false>);
   } else {
-    if (from_seed) go(prologue_kernel<double, C, MODE_GEN, true>);
-    else go(prologue_kernel<double, C, MODE_GEN, false>);
+    if (from_seed) m2 ? go(prologue_kernel<double, C, MD, true>) : go(prologue_kernel<double, C, MODE_GEN, true>);
+    else m2 ? go(prologue_kernel<double, C, MD, false>) : go(prologue_kernel<double, C, MODE_GEN, false>);
   }
   return cudaGetLastError();
 }
@@ -473,7 +510,7 @@ cudaError_t launch_epilogue_c(int xkind, int mode, const EpilogueArgs& a, int sm
 
 #define FCM_INSTANTIATE(C)                                                                        \
   template cudaError_t launch_pass_c<C>(int, int, const PassArgs&, int, cudaStream_t, int*, int, int); \
-  template cudaError_t launch_prologue_c<C>(int, bool, const PassArgs&, int, cudaStream_t);      \
+  template cudaError_t launch_prologue_c<C>(int, int, bool, const PassArgs&, int, cudaStream_t); \
   template cudaError_t launch_epilogue_c<C>(int, int, const EpilogueArgs&, int, cudaStream_t);
 
 }  // namespace fcm

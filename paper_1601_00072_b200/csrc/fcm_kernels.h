@@ -31,6 +31,9 @@ struct PassArgs {
   unsigned* oct_cnt;      // [noct]
   Control* ctl;
   double* trace;          // [max_iters]
+  cudaGraphConditionalHandle cond;  // device-side loop: while(cond) { pass } (graph mode)
+  int use_cond;
+  int finalize_local;     // 1: the CTA completing the rank root finalizes (single-rank jobs)
 };
 
 struct FinalizeArgs {
@@ -41,6 +44,8 @@ struct FinalizeArgs {
   int prologue;
   Control* ctl;
   double* trace;
+  cudaGraphConditionalHandle cond;
+  int use_cond;
 };
 
 struct EpilogueArgs {
@@ -57,7 +62,7 @@ struct EpilogueArgs {
 // variant 0: TMA bulk-copy pipeline (default); 1: register-staged LDG kernel.
 cudaError_t launch_pass(int xkind, int c, int mode, const PassArgs& a, int sms, cudaStream_t st,
                         int* grid_out, int variant = 0, int force_grid = 0);
-cudaError_t launch_prologue(int xkind, int c, bool from_seed, const PassArgs& a, int sms,
+cudaError_t launch_prologue(int xkind, int c, int mode, bool from_seed, const PassArgs& a, int sms,
                             cudaStream_t st);
 cudaError_t launch_epilogue(int xkind, int c, int mode, const EpilogueArgs& a, int sms,
                             cudaStream_t st);

@@ -150,16 +150,36 @@ __device__ __forceinline__ void voxel_general(double xd, const double* v, int c,
   }
 }
 
-template <typename XT, int C>
+// Per-pass intensity table for uint8 pixels (MODE_LUT): the Eq. 4 / Eq. 3
+// per-voxel terms are a function of the intensity alone, so each CTA
+// evaluates them once per pass for the 256 intensities (the same robust
+// fp64 formula the direct path uses, so values are identical) and the
+// stream then gathers them.  Rows are interleaved by 16-byte chunk
+// (chunk k of intensity b at (k*256 + b)*16) so lanes with different
+// intensities spread over the banks and equal intensities broadcast.
+template <int C>
+struct LutLayout {
+  static constexpr int K4 = (C + 3) / 4;  // float4 chunks of u (fp32) and of its residual
+  static constexpr int K2 = (C + 1) / 2;  // double2 chunks of w = u^m
+  static constexpr int kUfOff = 0;
+  static constexpr int kDuOff = kUfOff + K4 * 256 * 16;
+  static constexpr int kWOff = kDuOff + K4 * 256 * 16;
+  static constexpr int kJOff = kWOff + K2 * 256 * 16;
+  static constexpr int kBytes = kJOff + 256 * 8;
+};
+
+template <typename XT, int C, bool LUT = false>
 struct TmaLayout {
   static constexpr int kXBytes = kChunk * (int)sizeof(XT);
   static constexpr int kUBytes = kChunk * 4;
   static constexpr int kStageBytes = kXBytes + C * kUBytes;
-  static constexpr int kStages0 = kStageBudget / kStageBytes;
+  static constexpr int kLutBytes = LUT ? LutLayout<C>::kBytes : 0;
+  static constexpr int kStages0 = (kStageBudget - kLutBytes) / kStageBytes;
   static constexpr int kStages = kStages0 < 2 ? 2 : (kStages0 > 8 ? 8 : kStages0);
   static constexpr int kRingBytes = kStages * kStageBytes;
-  // ring | full[S] | empty[S] | meta[S]
-  static constexpr int kBarOff = kRingBytes;
+  // ring | lut | full[S] | empty[S] | meta[S]
+  static constexpr int kLutOff = kRingBytes;
+  static constexpr int kBarOff = kLutOff + kLutBytes;
   static constexpr int kMetaOff = kBarOff + 16 * kStages;
   static constexpr int kSmemBytes = kMetaOff + 16 * kStages;
 };
@@ -173,13 +193,12 @@ struct StageMeta {
 
 template <typename XT, int C, int MODE>
 __global__ void __launch_bounds__(kTmaThreads, 2) pass_tma_kernel(PassArgs a) {
-  using L = TmaLayout<XT, C>;
+  constexpr bool LUT = MODE == MODE_LUT;
+  using L = TmaLayout<XT, C, LUT>;
   constexpr int S = L::kStages;
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ SmemRedT<2 * C + 2> sm;
-  if (threadIdx.x == 0) sm.flag = *(volatile int*)&a.ctl->done;
-  __syncthreads();
-  if (sm.flag) return;
+  if (pass_done(a, sm)) return;
 
   const int tid = threadIdx.x;
   const uint32_t bar0 = smem_u32(smem + L::kBarOff);
@@ -249,6 +268,44 @@ __global__ void __launch_bounds__(kTmaThreads, 2) pass_tma_kernel(PassArgs a) {
 #pragma unroll
   for (int j = 0; j < C; ++j) v[j] = j < c ? a.ctl->v[j] : 0.0;
   const Powers pw = load_powers(a);
+  using LL = LutLayout<C>;
+  uint8_t* lut = smem + L::kLutOff;
+  if (LUT) {
+    // entry b = tid: the same robust Eq. 4 evaluation as the direct path
+    const double xb = (double)tid;
+    double u[C];
+    membership<C, MODE_GEN>(xb, v, c, pw, u);
+    double jt = 0.0;
+    float ufv[4 * LL::K4], duv[4 * LL::K4];
+    double wv[2 * LL::K2];
+#pragma unroll
+    for (int j = 0; j < 4 * LL::K4; ++j) ufv[j] = duv[j] = 0.0f;
+#pragma unroll
+    for (int j = 0; j < 2 * LL::K2; ++j) wv[j] = 0.0;
+#pragma unroll
+    for (int j = 0; j < C; ++j) {
+      const double w = pow_m<MODE_GEN>(u[j], pw);
+      const double d = xb - v[j];
+      jt = fma(w, d * d, jt);
+      wv[j] = w;
+      ufv[j] = (float)u[j];
+      duv[j] = (float)(u[j] - (double)ufv[j]);
+    }
+#pragma unroll
+    for (int k = 0; k < LL::K4; ++k) {
+      reinterpret_cast<float4*>(lut + LL::kUfOff)[k * 256 + tid] =
+          make_float4(ufv[4 * k], ufv[4 * k + 1], ufv[4 * k + 2], ufv[4 * k + 3]);
+      reinterpret_cast<float4*>(lut + LL::kDuOff)[k * 256 + tid] =
+          make_float4(duv[4 * k], duv[4 * k + 1], duv[4 * k + 2], duv[4 * k + 3]);
+    }
+#pragma unroll
+    for (int k = 0; k < LL::K2; ++k)
+      reinterpret_cast<double2*>(lut + LL::kWOff)[k * 256 + tid] = make_double2(wv[2 * k], wv[2 * k + 1]);
+    reinterpret_cast<double*>(lut + LL::kJOff)[tid] = jt;
+    red_sync<true>();
+  }
+  float dmax_f = 0.0f;
+  int tile_parity = 0;
   double acc[2 * C + 2];
 #pragma unroll
   for (int s = 0; s < 2 * C + 2; ++s) acc[s] = 0.0;
@@ -292,7 +349,36 @@ __global__ void __launch_bounds__(kTmaThreads, 2) pass_tma_kernel(PassArgs a) {
 #pragma unroll
       for (int j = 0; j < C; ++j) uq[j] = f4get(uo[j], q);
       const bool valid = q < nleft;
-      if (MODE == MODE_M2 && sizeof(XT) == 1 && C <= 8)
+      if (LUT) {
+        const int b = (int)(xd[q] - 0.0);
+        float ufv[4 * LL::K4], duv[4 * LL::K4];
+        double wv[2 * LL::K2];
+#pragma unroll
+        for (int k = 0; k < LL::K4; ++k) {
+          const float4 f = reinterpret_cast<const float4*>(lut + LL::kUfOff)[k * 256 + b];
+          const float4 e = reinterpret_cast<const float4*>(lut + LL::kDuOff)[k * 256 + b];
+          ufv[4 * k] = f.x; ufv[4 * k + 1] = f.y; ufv[4 * k + 2] = f.z; ufv[4 * k + 3] = f.w;
+          duv[4 * k] = e.x; duv[4 * k + 1] = e.y; duv[4 * k + 2] = e.z; duv[4 * k + 3] = e.w;
+        }
+#pragma unroll
+        for (int k = 0; k < LL::K2; ++k) {
+          const double2 w2 = reinterpret_cast<const double2*>(lut + LL::kWOff)[k * 256 + b];
+          wv[2 * k] = w2.x;
+          wv[2 * k + 1] = w2.y;
+        }
+        if (valid) acc[2 * C] += reinterpret_cast<const double*>(lut + LL::kJOff)[b];
+#pragma unroll
+        for (int j = 0; j < C; ++j) {
+          // |u - u_old| = |(fl32(u) - u_old) + (u - fl32(u))|, both fp32-exact to ~1e-12
+          const float dl = fabsf((ufv[j] - uq[j]) + duv[j]);
+          if (valid) {
+            acc[j] = fma(wv[j], xd[q], acc[j]);
+            acc[C + j] += wv[j];
+            dmax_f = fmaxf(dmax_f, dl);
+          }
+          nq[j] = ufv[j];
+        }
+      } else if (MODE == MODE_M2 && sizeof(XT) == 1 && C <= 8)
         voxel_m2_u8<C>(xd[q], v, uq, nq, acc, dmax_hi, valid);
       else
         voxel_general<C, MODE>(xd[q], v, c, pw, uq, nq, acc, dmax_hi, valid);
@@ -303,12 +389,13 @@ __global__ void __launch_bounds__(kTmaThreads, 2) pass_tma_kernel(PassArgs a) {
     for (int j = 0; j < C; ++j)
       if (j < c) __stcs(reinterpret_cast<float4*>(a.u_nxt + j * a.g.plane + i0), un[j]);
     if (mt.last) {
-      acc[2 * C + 1] = __hiloint2double((int)dmax_hi, (int)0xffffffffu);
-      tile_finish<C, true>(a, mt.tile, acc, sm, false);
-      red_sync<true>();
+      acc[2 * C + 1] = LUT ? (double)dmax_f : __hiloint2double((int)dmax_hi, (int)0xffffffffu);
+      tile_finish<C, true>(a, mt.tile, acc, sm, false, tile_parity);
+      tile_parity ^= 1;
 #pragma unroll
       for (int s = 0; s < 2 * C + 2; ++s) acc[s] = 0.0;
       dmax_hi = 0;
+      dmax_f = 0.0f;
     }
   }
 }
@@ -316,7 +403,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) pass_tma_kernel(PassArgs a) {
 template <typename XT, int C, int MODE>
 inline cudaError_t launch_pass_tma(const PassArgs& a, int sms, cudaStream_t st, int* grid_out,
                                    int force_grid) {
-  using L = TmaLayout<XT, C>;
+  using L = TmaLayout<XT, C, MODE == MODE_LUT>;
   auto k = pass_tma_kernel<XT, C, MODE>;
   int dev = 0;
   cudaGetDevice(&dev);

@@ -19,6 +19,7 @@ computes on the CPU except argument validation and result packaging.
 from __future__ import annotations
 
 import ctypes
+import os
 
 import numpy as np
 
@@ -81,9 +82,25 @@ class FcmPlan:
         info = self.info()
         self.n_local, self.voxel0 = info["n_local"], info["voxel0"]
 
+    @staticmethod
+    def _locate_nccl():
+        """Point the C library at the wheel's libnccl (it dlopens on first use)."""
+        if os.environ.get("FCM_NCCL_LIB"):
+            return
+        try:
+            import nvidia.nccl
+            for d in nvidia.nccl.__path__:
+                cand = os.path.join(d, "lib", "libnccl.so.2")
+                if os.path.exists(cand):
+                    os.environ["FCM_NCCL_LIB"] = cand
+                    return
+        except ImportError:
+            pass
+
     @classmethod
     def for_rank(cls, n_global: int, c: int, x_kind: int, device: int, nranks: int, rank: int,
                  nccl_id: bytes | None = None):
+        cls._locate_nccl()
         h = ctypes.c_void_p()
         idbuf = ctypes.create_string_buffer(nccl_id, 128) if nccl_id else None
         check(lib().fcm_plan_create_rank(ctypes.byref(h), int(n_global), int(c), int(x_kind), int(device),
@@ -92,6 +109,7 @@ class FcmPlan:
 
     @staticmethod
     def nccl_unique_id() -> bytes:
+        FcmPlan._locate_nccl()
         buf = ctypes.create_string_buffer(128)
         check(lib().fcm_nccl_unique_id(buf), None, "fcm_nccl_unique_id")
         return buf.raw

@@ -76,3 +76,13 @@ def test_delta_and_argmax_vs_reference():
     b = pkg.MembershipMatrix(257, 3, u[::-1].copy())
     assert pkg.membership_delta(a, b) == k["k_maxdiff"][0]
     assert np.array_equal(pkg.defuzzify(a, 257, 1).labels, k["k_argmax"])
+
+
+@pytest.mark.parametrize("n,c,seed", [(3_000_000, 3, 0), (700_000, 8, 12345), (500_000, 5, 2**63 + 7)])
+def test_init_membership_large_bitwise(n, c, seed):
+    """Device SplitMix64 rows (shared-reciprocal IEEE quotients) == reference generator, bit for bit."""
+    from oracle import oracle as O
+    s = seed if seed < 2**63 else seed - 2**64
+    got = pkg.init_membership(n, pkg.FcmConfig(c=c, seed=s)).u
+    ref = O.fill_membership_random(n, c, seed)
+    assert got.tobytes() == ref.tobytes()

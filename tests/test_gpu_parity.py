@@ -141,3 +141,91 @@ def test_iterate_matches_reference_contract():
     assert k == r["iterations"] and conv == r["converged"] and len(trace) == k
     assert np.allclose(v, r["v"], rtol=CENTER_RTOL)
     assert np.abs(u - r["u"]).max() <= U_ATOL
+
+
+@pytest.mark.parametrize("kernel,graph", [(0, 0), (1, 1), (1, 0), (2, 1)])
+def test_launch_modes_and_kernels_agree(kernel, graph):
+    """Device-side loop (CUDA graph + conditional node) vs host-driven batches,
+    and the TMA / register-staged / intensity-table pass kernels: same run."""
+    from paper_1601_00072_b200 import _lib
+    r = run_case("phantom_c4")
+    x = r["x"].astype(np.uint8)
+
+    def solve(kernel, graph):
+        with pkg.FcmPlan(x.shape[0], 4, _lib.FCM_X_U8) as plan:
+            plan.upload_pixels(x)
+            plan.init_membership(r["seed"])
+            plan.set_option(_lib.FCM_OPT_KERNEL, kernel)
+            plan.set_option(_lib.FCM_OPT_GRAPH, graph)
+            v, trace, k, conv = plan.run(2.0, r["epsilon"], r["max_iters"])
+            u, lab = plan.download()
+        return v, trace, k, conv, u, lab
+
+    base = solve(0, 1)
+    other = solve(kernel, graph)
+    assert other[2] == base[2] == r["iterations"] and other[3] == base[3]
+    assert np.allclose(other[0], base[0], rtol=1e-12)
+    assert np.array_equal(other[5], base[5])
+    if kernel == 0:
+        assert other[0].tobytes() == base[0].tobytes() and other[1].tobytes() == base[1].tobytes()
+
+
+def test_graph_loop_reuse_and_max_iters():
+    # the cached graph must honour a new max_iters / epsilon and restart cleanly
+    from paper_1601_00072_b200 import _lib
+    r = run_case("C1")
+    x = r["x"].astype(np.uint8)
+    with pkg.FcmPlan(x.shape[0], 3, _lib.FCM_X_U8) as plan:
+        plan.upload_pixels(x)
+        plan.init_membership(0)
+        a = plan.run(2.0, 1e-5, 500)
+        b = plan.run(2.0, 1e-5, 7)
+        c = plan.run(2.0, 1e-5, 500)
+        assert a[2] == r["iterations"] and b[2] == 7 and not b[3] and c[2] == a[2]
+        assert a[0].tobytes() == c[0].tobytes()
+        assert np.array_equal(b[1], a[1][:7])
+
+
+@pytest.mark.parametrize("graph", [1, 0])
+def test_nccl_exchange_path_single_rank(graph):
+    """Roots through a real (one-rank) NCCL communicator + the finalize kernel
+    == the in-kernel finalize of a local plan, bit for bit."""
+    from paper_1601_00072_b200 import _lib
+    r = run_case("C1")
+    x = r["x"].astype(np.uint8)
+    n = x.shape[0]
+
+    def solve(plan):
+        plan.upload_pixels(x)
+        plan.init_membership(0)
+        plan.set_option(_lib.FCM_OPT_GRAPH, graph)
+        v, trace, k, conv = plan.run(2.0, 1e-5, 500)
+        u, lab = plan.download()
+        plan.close()
+        return v, trace, k, conv, u, lab
+
+    local = solve(pkg.FcmPlan(n, 3, _lib.FCM_X_U8))
+    nccl = solve(pkg.FcmPlan.for_rank(n, 3, _lib.FCM_X_U8, 0, 1, 0, pkg.FcmPlan.nccl_unique_id()))
+    assert nccl[2] == local[2] == r["iterations"]
+    assert nccl[0].tobytes() == local[0].tobytes()
+    assert nccl[1].tobytes() == local[1].tobytes()
+    assert nccl[4].tobytes() == local[4].tobytes()
+
+
+def test_config2_volume_vs_oracle():
+    """BASELINE config 2 (181x217x181, 7.1M voxels, c=3, m=2, eps=1e-5) against
+    the oracle's block-parallel engine (bit-identical to the reference's
+    parallel._iterate; reference seq/par agree within the pins below)."""
+    from oracle import oracle as O
+    from paper_1601_00072_b200.phantom import make_config
+    x8 = make_config("C2")
+    x = x8.astype(np.float64)
+    ref = O.run_fcm(x, 3, 2.0, 1e-5, 500, 0, engine="parallel")
+    img = pkg.GrayImage(181, 217 * 181, x)
+    res = pkg.run_fcm_gpu(img, pkg.FcmConfig(c=3, m=2.0, epsilon=1e-5, seed=0))
+    assert res.iterations == ref["iterations"] == 14
+    assert res.converged == ref["converged"]
+    assert np.allclose(res.centers.v, ref["centers"], rtol=CENTER_RTOL)
+    assert np.abs(res.membership.u - ref["membership"]).max() <= U_ATOL
+    assert np.array_equal(res.labels.labels, ref["labels"])
+    assert np.allclose(np.array(res.objective_trace), ref["objective_trace"], rtol=TRACE_RTOL)
