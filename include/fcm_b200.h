@@ -57,9 +57,15 @@ typedef enum {
                           product form for m == 2, per-pass intensity table for other m on uint8),
                           1 = register-staged LDG/STG, 2 = TMA + intensity table for every m (uint8),
                           3 = TMA + per-voxel math for every m */
-  FCM_OPT_GRAPH = 5    /* 1 (default): single-shard runs launch prologue + a device-side while loop
-                          (CUDA graph conditional node) -- no host round trip per iteration;
+  FCM_OPT_GRAPH = 5,   /* 1 (default): when the loop kernel is off, single-shard runs launch
+                          prologue + a device-side while loop (CUDA graph conditional node);
                           0: host-driven batches.  FCM_OPT_TIMING forces the host-driven path. */
+  FCM_OPT_LOOP = 6,    /* 1 (default): single-shard, single-rank runs launch the prologue and ONE
+                          persistent cooperative kernel that runs every pass, with a grid barrier
+                          between passes; 0: one launch per pass (graph or host-driven) */
+  FCM_OPT_L2 = 7,      /* 0: stream x/u with evict-first stores; 1 (default): keep them in L2
+                          (evict_last policy) when they fit; 2: always */
+  FCM_OPT_PROFILE = 8  /* 1: the loop kernel records a per-CTA timeline (fcm_last_profile) */
 } fcm_option;
 
 typedef struct fcm_plan fcm_plan;
@@ -91,7 +97,7 @@ int fcm_nccl_unique_id(void* out128);
 
 /* Host-only: the voxel range and reduction-tree geometry of `rank` in an
  * nranks job over n voxels (no GPU needed).  out[0..]: n_local, voxel0,
- * tile voxels, tiles T, tiles per octant M, groups per octant, first octant,
+ * tile voxels, tiles T, tiles per octant M, tree levels per octant, first octant,
  * octants, first tile, tiles_local. */
 int fcm_geometry(int64_t n, int32_t nranks, int32_t rank, int64_t* out, int32_t count);
 
@@ -136,6 +142,12 @@ int fcm_download(fcm_plan* plan, double* u_aos_out, int32_t* labels_out);
  * events), mean ms per pass (when FCM_OPT_TIMING), prologue ms, passes
  * launched, passes that did work. */
 int fcm_last_timing(const fcm_plan* plan, double* out, int32_t count);
+
+/* Loop-kernel timeline of the last fcm_run with FCM_OPT_PROFILE (diagnostics):
+ * out[(pass * grid + cta) * 16 + k], k = 0 pass start, 1 producer done claiming,
+ * 2 consumers done, 3 grid barrier released (globaltimer ns), 4 tiles claimed.
+ * count must be >= passes * grid * 16; passes <= min(max_iters, 64). */
+int fcm_last_profile(const fcm_plan* plan, uint64_t* out, int64_t count, int32_t* passes, int32_t* grid);
 
 /* Page-lock caller memory so uploads/downloads run at full PCIe speed. */
 int fcm_host_register(void* ptr, int64_t bytes);

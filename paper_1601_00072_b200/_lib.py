@@ -12,11 +12,12 @@ import os
 
 from .errors import DegenerateClusterError, DeviceError, FcmError, InvalidConfigError
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libfcm_b200.so")
+LIB_PATH = os.environ.get("FCM_B200_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libfcm_b200.so")
 
 FCM_OK, FCM_E_ARG, FCM_E_CUDA, FCM_E_NCCL, FCM_E_DEGENERATE, FCM_E_STATE, FCM_E_NOMEM = range(7)
 FCM_X_U8, FCM_X_F64 = 0, 2
 FCM_OPT_BATCH, FCM_OPT_TIMING, FCM_OPT_GRID, FCM_OPT_KERNEL, FCM_OPT_GRAPH = 1, 2, 3, 4, 5
+FCM_OPT_LOOP, FCM_OPT_L2, FCM_OPT_PROFILE = 6, 7, 8
 
 # Every symbol the header declares (tests/test_abi.py checks the .so exports them).
 SIGNATURES = {
@@ -42,6 +43,8 @@ SIGNATURES = {
                  ctypes.POINTER(ctypes.c_int32)], ctypes.c_int),
     "fcm_download": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
     "fcm_last_timing": ([ctypes.c_void_p, ctypes.POINTER(ctypes.c_double), ctypes.c_int32], ctypes.c_int),
+    "fcm_last_profile": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.POINTER(ctypes.c_int32),
+                          ctypes.POINTER(ctypes.c_int32)], ctypes.c_int),
     "fcm_host_register": ([ctypes.c_void_p, ctypes.c_int64], ctypes.c_int),
     "fcm_host_unregister": ([ctypes.c_void_p], ctypes.c_int),
     "fcm_fill_membership_random": ([ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_uint64,
@@ -100,7 +103,7 @@ def ptr(a) -> ctypes.c_void_p:
     return ctypes.c_void_p(a.ctypes.data) if a is not None else ctypes.c_void_p(0)
 
 
-GEOMETRY_KEYS = ("n_local", "voxel0", "tile", "T", "M", "gpo", "oct0", "noct", "tile0", "tiles_local")
+GEOMETRY_KEYS = ("n_local", "voxel0", "tile", "T", "M", "levels", "oct0", "noct", "tile0", "tiles_local")
 
 
 def geometry(n: int, nranks: int = 1, rank: int = 0) -> dict:

@@ -65,15 +65,16 @@ struct Shard {
   cudaEvent_t ev_pass = nullptr;
   Geometry g{};
   void* x = nullptr;
-  float* u[2] = {nullptr, nullptr};
+  float* u = nullptr;  // fp32 SoA membership, updated in place pass after pass
+  int keep_l2 = 0;     // x + u fit in L2 (evict_last policy on the stream)
   double* u0_aos = nullptr;
   double* tile_part = nullptr;
-  double* group_root = nullptr;
-  double* oct_root = nullptr;
+  double* node_part[kMaxLevels + 1] = {};  // level l >= 1: [noct][nodes[l]][nf]
+  double* l1_buf = nullptr;                // loop kernel: [2][noct][nodes[1]][nf]
   double* rank_root = nullptr;  // [2][nf], double-buffered by pass parity
   double* gathered = nullptr;   // [nranks][nf] (NCCL)
-  unsigned* group_cnt = nullptr;
-  unsigned* oct_cnt = nullptr;
+  unsigned* node_cnt[kMaxLevels + 1] = {};
+  size_t cnt_total = 0;  // counters of all levels, one allocation (node_cnt[1] is its base)
   Control* ctl = nullptr;
   double* trace = nullptr;
   int trace_cap = 0;
@@ -107,13 +108,20 @@ struct fcm_plan {
   // graph mode: prologue + while(!done) { pass; pass } as ONE CUDA graph with a
   // device-side conditional loop -- no host round trip per iteration
   int use_graph = 1;
+  // loop mode: prologue + ONE persistent cooperative kernel running every
+  // pass with grid barriers in between (single-shard, single-rank plans)
+  int use_loop = 1;
+  int l2_mode = 1;  // 0 never keep x/u in L2, 1 when they fit (default), 2 always
+  int profile = 0;  // record the loop kernel's per-CTA timeline
+  uint64_t* prof = nullptr;
+  int prof_passes = 0, prof_grid = 0;
   bool capturing = false;
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t gexec = nullptr;
   cudaGraphConditionalHandle gcond = 0;
   struct GraphKey {
     double m, eps;
-    int max_iters, init_src, variant, force_grid;
+    int max_iters, init_src, variant, force_grid, l2_mode;
     uint64_t seed;
   } gkey{};
   Control* host_ctl = nullptr;   // pinned: device -> host reads of the control block
@@ -152,10 +160,16 @@ int nf_of(int c) { return 2 * c + 2; }
 int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 // Global tile tree ("Deterministic reduction").  Depends only on n.
+// Tile = the smallest power of two >= 1024 voxels (>= 2048 once the volume
+// gives a full B200 -- 2 x 148 CTAs -- 8 tiles per CTA) that keeps the tile
+// count <= 64 per CTA: enough tiles that the end-of-pass imbalance (<= one
+// tile) stays short, few enough that per-tile reduction work stays small.
+// Beyond 8 * 32^3 tiles they grow further.
 void base_geometry(int64_t n, Geometry& g) {
-  int64_t tile = 1024;
-  while (tile < ceil_div(n, 8192)) tile <<= 1;
-  while (tile < 4096 && n / tile > 2048) tile <<= 1;
+  int64_t tile = n >= int64_t(2048) * 8 * 296 ? 2048 : 1024;
+  while (ceil_div(n, tile) > int64_t(64) * 296) tile <<= 1;
+  const int64_t cap = (int64_t)kOctants << (5 * kMaxLevels);
+  while (ceil_div(n, tile) > cap) tile <<= 1;
   int shift = 0;
   while ((int64_t(1) << shift) < tile) ++shift;
   g.n_global = n;
@@ -163,7 +177,10 @@ void base_geometry(int64_t n, Geometry& g) {
   g.T = (int)ceil_div(n, tile);
   const int T8 = (int)ceil_div(g.T, kOctants) * kOctants;
   g.M = T8 / kOctants;
-  g.gpo = (int)ceil_div(g.M, kGroup);
+  g.levels = 1;
+  while ((int64_t(1) << (5 * g.levels)) < g.M) ++g.levels;
+  for (int l = 0; l <= kMaxLevels; ++l)
+    g.nodes[l] = l <= g.levels ? (int)ceil_div(g.M, int64_t(1) << (5 * l)) : 0;
 }
 
 void rank_geometry(Geometry& g, int nranks, int rank) {
@@ -215,19 +232,32 @@ int setup_shard(fcm_plan* p, Shard& s) {
   if ((rc = dalloc(p, s, &xb, s.g.plane * xsz))) return rc;
   s.x = xb;
   CK(cudaMemsetAsync(s.x, 0, s.g.plane * xsz, s.stream));
-  for (int b = 0; b < 2; ++b)
-    if ((rc = dalloc(p, s, &s.u[b], (size_t)s.g.plane * p->c))) return rc;
+  if ((rc = dalloc(p, s, &s.u, (size_t)s.g.plane * p->c))) return rc;
+  const double resident = (double)s.g.plane * (double)(xsz + 4 * p->c);
+  s.keep_l2 = resident <= 0.8 * (double)prop.l2CacheSize ? 1 : 0;
   if ((rc = dalloc(p, s, &s.tile_part, (size_t)std::max(s.g.tiles_local, 1) * nf))) return rc;
-  if ((rc = dalloc(p, s, &s.group_root, (size_t)s.g.noct * s.g.gpo * nf))) return rc;
-  if ((rc = dalloc(p, s, &s.oct_root, (size_t)s.g.noct * nf))) return rc;
+  size_t cnt_total = 0;
+  for (int l = 1; l <= s.g.levels; ++l) {
+    if ((rc = dalloc(p, s, &s.node_part[l], (size_t)s.g.noct * s.g.nodes[l] * nf))) return rc;
+    cnt_total += (size_t)s.g.noct * s.g.nodes[l];
+  }
   if ((rc = dalloc(p, s, &s.rank_root, (size_t)2 * nf))) return rc;
   if ((rc = dalloc(p, s, &s.gathered, (size_t)p->nranks * nf))) return rc;
-  if ((rc = dalloc(p, s, &s.group_cnt, (size_t)s.g.noct * s.g.gpo))) return rc;
-  if ((rc = dalloc(p, s, &s.oct_cnt, (size_t)s.g.noct))) return rc;
+  if ((rc = dalloc(p, s, &s.l1_buf, (size_t)2 * s.g.noct * s.g.nodes[1] * nf))) return rc;
+  unsigned* cnt = nullptr;
+  if ((rc = dalloc(p, s, &cnt, cnt_total))) return rc;
+  s.cnt_total = cnt_total;
+  for (int l = 1; l <= s.g.levels; ++l) {
+    s.node_cnt[l] = cnt;
+    cnt += (size_t)s.g.noct * s.g.nodes[l];
+  }
   if ((rc = dalloc(p, s, &s.ctl, 1))) return rc;
-  CK(cudaMemsetAsync(s.group_cnt, 0, sizeof(unsigned) * s.g.noct * s.g.gpo, s.stream));
-  CK(cudaMemsetAsync(s.oct_cnt, 0, sizeof(unsigned) * s.g.noct, s.stream));
+  CK(cudaMemsetAsync(s.node_cnt[1], 0, sizeof(unsigned) * s.cnt_total, s.stream));
   CK(cudaMemsetAsync(s.ctl, 0, sizeof(Control), s.stream));
+  // every tree slot starts unpublished (all-ones NaN pattern, see fcm_kernels.cuh)
+  CK(cudaMemsetAsync(s.tile_part, 0xff, sizeof(double) * std::max(s.g.tiles_local, 1) * nf, s.stream));
+  for (int l = 1; l <= s.g.levels; ++l)
+    CK(cudaMemsetAsync(s.node_part[l], 0xff, sizeof(double) * s.g.noct * s.g.nodes[l] * nf, s.stream));
   return FCM_OK;
 }
 
@@ -315,8 +345,8 @@ PassArgs make_args(fcm_plan* p, Shard& s, int seq, double eps, int max_iters) {
   PassArgs a{};
   const int nf = nf_of(p->c);
   a.x = s.x;
-  a.u_cur = s.u[(seq + 1) & 1];  // pass seq reads u[(seq-1)&1]
-  a.u_nxt = s.u[seq & 1];        // prologue (seq 0) writes u[0]
+  a.u_cur = s.u;  // in place: each element is read before the same thread rewrites it
+  a.u_nxt = s.u;
   a.u0_aos = s.u0_aos;
   a.seed = p->seed;
   a.c = p->c;
@@ -331,16 +361,18 @@ PassArgs make_args(fcm_plan* p, Shard& s, int seq, double eps, int max_iters) {
   a.seq = seq;
   a.g = s.g;
   a.tile_part = s.tile_part;
-  a.group_root = s.group_root;
-  a.oct_root = s.oct_root;
+  for (int l = 0; l <= kMaxLevels; ++l) {
+    a.node_part[l] = s.node_part[l];
+    a.node_cnt[l] = s.node_cnt[l];
+  }
   a.rank_root = s.rank_root + (seq & 1) * nf;
-  a.group_cnt = s.group_cnt;
-  a.oct_cnt = s.oct_cnt;
   a.ctl = s.ctl;
   a.trace = s.trace;
   a.cond = p->gcond;
   a.use_cond = p->capturing ? 1 : 0;
   a.finalize_local = (p->nranks == 1 && !p->use_nccl) ? 1 : 0;
+  a.keep_l2 = p->l2_mode == 2 ? 1 : (p->l2_mode == 1 ? s.keep_l2 : 0);
+  a.l1_buf = s.l1_buf;
   return a;
 }
 
@@ -560,7 +592,7 @@ int fcm_geometry(int64_t n, int32_t nranks, int32_t rank, int64_t* out, int32_t 
   base_geometry(n, g);
   rank_geometry(g, nranks, rank);
   const int64_t v[] = {g.n_local, g.voxel0, int64_t(1) << g.tile_shift, g.T, g.M,
-                       g.gpo, g.oct0, g.noct, g.tile0, g.tiles_local};
+                       g.levels, g.oct0, g.noct, g.tile0, g.tiles_local};
   for (int i = 0; i < count && i < (int)(sizeof v / sizeof v[0]); ++i) out[i] = v[i];
   return FCM_OK;
 }
@@ -639,6 +671,12 @@ int fcm_set_option(fcm_plan* p, int32_t key, int64_t value) {
       p->force_grid = (int)value;
       return FCM_OK;
     case FCM_OPT_GRAPH: p->use_graph = value ? 1 : 0; return FCM_OK;
+    case FCM_OPT_LOOP: p->use_loop = value ? 1 : 0; return FCM_OK;
+    case FCM_OPT_PROFILE: p->profile = value ? 1 : 0; return FCM_OK;
+    case FCM_OPT_L2:
+      if (value < 0 || value > 2) return FCM_E_ARG;
+      p->l2_mode = (int)value;
+      return FCM_OK;
     case FCM_OPT_KERNEL:
       if (value < 0 || value > 3) return FCM_E_ARG;
       p->variant = (int)value;
@@ -735,15 +773,52 @@ int fcm_run(fcm_plan* p, double m, double eps, int32_t max_iters, double* v_out,
       s.trace_cap = max_iters;
     }
     CK(cudaMemcpyAsync(s.ctl, p->host_tmpl, sizeof(Control), cudaMemcpyHostToDevice, s.stream));
-    CK(cudaMemsetAsync(s.group_cnt, 0, sizeof(unsigned) * s.g.noct * s.g.gpo, s.stream));
-    CK(cudaMemsetAsync(s.oct_cnt, 0, sizeof(unsigned) * s.g.noct, s.stream));
+    CK(cudaMemsetAsync(s.node_cnt[1], 0, sizeof(unsigned) * s.cnt_total, s.stream));
+    const int nf = nf_of(p->c);
+    CK(cudaMemsetAsync(s.tile_part, 0xff, sizeof(double) * std::max(s.g.tiles_local, 1) * nf, s.stream));
+    for (int l = 1; l <= s.g.levels; ++l)
+      CK(cudaMemsetAsync(s.node_part[l], 0xff, sizeof(double) * s.g.noct * s.g.nodes[l] * nf, s.stream));
   }
   Shard& s0 = p->sh[0];
   CK(cudaSetDevice(s0.device));
   p->passes_launched = 0;
   int rc = FCM_OK;
-  const bool graph = p->use_graph && p->nshards == 1 && !p->timing;
-  if (graph) {
+  const bool single = p->nshards == 1 && !p->use_nccl && !p->timing;
+  bool loop = single && p->use_loop && p->variant != 1 && s0.g.tiles_local > 0;
+  const bool graph = !loop && single && p->use_graph;
+  bool looped = false;
+  if (loop) {
+    CK(cudaEventRecord(p->ev_start, s0.stream));
+    if ((rc = step(p, 0, eps, max_iters))) return rc;
+    CK(cudaEventRecord(p->ev_pro, s0.stream));
+    PassArgs a = make_args(p, s0, 1, eps, max_iters);
+    if (p->profile) {
+      const int passes = std::min(max_iters, 64);
+      if (!p->prof) {
+        int rc2 = dalloc(p, s0, &p->prof, (size_t)64 * 2 * s0.sms * 4 * kProbeSlots);
+        if (rc2) return rc2;
+      }
+      CK(cudaMemsetAsync(p->prof, 0, sizeof(uint64_t) * 64 * 2 * s0.sms * 4 * kProbeSlots, s0.stream));
+      a.prof = p->prof;
+      a.prof_passes = passes;
+      p->prof_passes = passes;
+    }
+    int grid = 0;
+    cudaError_t e = launch_loop(p->xkind, p->c, p->mode, a, s0.sms, s0.stream, &grid, p->variant, p->force_grid);
+    if (e == cudaSuccess) {
+      s0.last_grid = grid;
+      p->prof_grid = grid;
+      p->passes_launched = 1;
+      looped = true;
+    } else if (e == cudaErrorCooperativeLaunchTooLarge || e == cudaErrorNotSupported) {
+      cudaGetLastError();  // grid cannot be co-resident: host-driven passes below
+    } else {
+      CK(e);
+    }
+  }
+  if (looped) {
+    // nothing else to enqueue: the loop kernel ran every pass
+  } else if (graph) {
     fcm_plan::GraphKey key;
     memset(&key, 0, sizeof key);  // padding takes part in the memcmp below
     key.m = m;
@@ -752,6 +827,7 @@ int fcm_run(fcm_plan* p, double m, double eps, int32_t max_iters, double* v_out,
     key.init_src = p->init_src;
     key.variant = p->variant;
     key.force_grid = p->force_grid;
+    key.l2_mode = p->l2_mode;
     key.seed = p->seed;
     if (!p->gexec || memcmp(&key, &p->gkey, sizeof key) != 0) {
       if ((rc = build_graph(p, eps, max_iters))) return rc;
@@ -761,11 +837,13 @@ int fcm_run(fcm_plan* p, double m, double eps, int32_t max_iters, double* v_out,
     CK(cudaGraphLaunch(p->gexec, s0.stream));
     CK(cudaEventRecord(p->ev_pro, s0.stream));
   } else {
-    CK(cudaEventRecord(p->ev_start, s0.stream));
-    rc = step(p, 0, eps, max_iters);
-    if (rc) return rc;
-    CK(cudaSetDevice(s0.device));
-    CK(cudaEventRecord(p->ev_pro, s0.stream));
+    if (!loop) {
+      CK(cudaEventRecord(p->ev_start, s0.stream));
+      rc = step(p, 0, eps, max_iters);
+      if (rc) return rc;
+      CK(cudaSetDevice(s0.device));
+      CK(cudaEventRecord(p->ev_pro, s0.stream));
+    }
     int seq = 1;
     while (seq <= max_iters) {
       const int nb = std::min(p->batch, max_iters - seq + 1);
@@ -794,6 +872,11 @@ int fcm_run(fcm_plan* p, double m, double eps, int32_t max_iters, double* v_out,
   p->passes_done = h.iter;
   if (graph) p->passes_launched = (int)h.launches;
   p->t_pass_ms = 0;
+  if (looped && h.iter > 0) {
+    // the loop kernel's own duration per pass (barriers included)
+    CK(cudaEventElapsedTime(&ms, p->ev_pro, p->ev_end));
+    p->t_pass_ms = ms / h.iter;
+  }
   if (p->timing && h.iter > 0) {
     double tot = 0;
     for (int k = 0; k < h.iter && k < (int)p->ev_t0.size(); ++k) {
@@ -810,6 +893,7 @@ int fcm_run(fcm_plan* p, double m, double eps, int32_t max_iters, double* v_out,
     CK(cudaMemcpy(trace_out, s0.trace, sizeof(double) * h.iter, cudaMemcpyDeviceToHost));
   if (!h.done) return fail(p, FCM_E_STATE, "loop ended without the done flag");
   if (h.dead == -2) return fail(p, FCM_E_STATE, "device loop watchdog fired (internal error)");
+  if (h.dead == -3) return fail(p, FCM_E_STATE, "loop kernel grid barrier timed out (internal error)");
   if (h.dead >= 0) return fail(p, FCM_E_DEGENERATE, "cluster %d has zero total membership weight", h.dead);
   p->run_ok = true;
   return FCM_OK;
@@ -860,6 +944,17 @@ int fcm_last_timing(const fcm_plan* p, double* out, int32_t count) {
   const double v[] = {p->t_loop_ms, p->t_pass_ms, p->t_pro_ms, (double)p->passes_launched,
                       (double)p->passes_done};
   for (int i = 0; i < count && i < (int)(sizeof v / sizeof v[0]); ++i) out[i] = v[i];
+  return FCM_OK;
+}
+
+int fcm_last_profile(const fcm_plan* p, uint64_t* out, int64_t count, int32_t* passes, int32_t* grid) {
+  if (!p || !out) return FCM_E_ARG;
+  if (!p->prof || !p->prof_grid) return FCM_E_STATE;
+  const int64_t want = (int64_t)p->prof_passes * p->prof_grid * kProbeSlots;
+  if (count < want) return FCM_E_ARG;
+  if (cudaMemcpy(out, p->prof, sizeof(uint64_t) * want, cudaMemcpyDeviceToHost) != cudaSuccess) return FCM_E_CUDA;
+  if (passes) *passes = p->prof_passes;
+  if (grid) *grid = p->prof_grid;
   return FCM_OK;
 }
 
@@ -950,8 +1045,7 @@ int fcm_update_centers(const double* x, const double* u, double* v_out, int64_t 
     if (!rc) {
       *p->host_tmpl = tmpl;
       cudaMemcpyAsync(s.ctl, p->host_tmpl, sizeof tmpl, cudaMemcpyHostToDevice, s.stream);
-      cudaMemsetAsync(s.group_cnt, 0, sizeof(unsigned) * s.g.noct * s.g.gpo, s.stream);
-      cudaMemsetAsync(s.oct_cnt, 0, sizeof(unsigned) * s.g.noct, s.stream);
+      cudaMemsetAsync(s.node_cnt[1], 0, sizeof(unsigned) * s.cnt_total, s.stream);
       rc = step(p, 0, 0.5, 1);
       if (!rc && cudaStreamSynchronize(s.stream) != cudaSuccess) rc = FCM_E_CUDA;
     }

@@ -22,6 +22,7 @@ namespace fcm {
 template <int NF>
 struct SmemRedT {
   double w[2][kWarps][NF];
+  double part[NF];
   double root[NF];
   int tile;
   int flag;
@@ -113,26 +114,132 @@ __device__ __forceinline__ bool pass_done(const PassArgs& a, SM& sm) {
 // arrivals' stores visible.  Replaces a full __threadfence on every thread.
 __device__ __forceinline__ unsigned atom_add_acq_rel(unsigned* p, unsigned v) {
   unsigned old;
+#ifdef FCM_EXPERIMENT_RELAXED
+  asm volatile("atom.add.relaxed.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+#else
   asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+#endif
   return old;
 }
 
-// Reduce the per-thread payload of local tile lt to the tile partial, then
-// climb the tree: the CTA that completes a group of 32 tiles reduces the
-// group, the one that completes an octant reduces the octant, the one that
-// completes the rank reduces the rank (and finalizes when it is alone).
-// Only warp 0 goes past the first barrier, so the other warps return to the
-// stream at once; `buf` double-buffers the per-warp scratch for that reason.
-// Lane 0 writes every tree node it publishes, so its acq_rel counter update
-// orders exactly the stores it covers.
+// ---------------------------------------------------- publish protocol ----
+// Every tree node slot (tile partials and node results) holds the all-ones
+// NaN bit pattern while unpublished: no tree value can be that NaN (sums of
+// finite terms and a max of |differences|).  The TMA kernels publish with
+// relaxed device-scope stores and their fixed owners poll for the pattern to
+// disappear -- no fence or atomic per tile; every reader writes the pattern
+// back once it has consumed a slot, so the next pass starts clean.
+__device__ __forceinline__ double sentinel() { return __longlong_as_double(-1ll); }
+__device__ __forceinline__ bool is_sentinel(double v) { return __double_as_longlong(v) == -1ll; }
+__device__ __forceinline__ void st_relaxed(double* p, double v) {
+  asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+__device__ __forceinline__ double ld_relaxed(const double* p) {
+  double v;
+  asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// ----------------------------------------------------------- the climb ----
+// One warp completes node `node` of level l >= 1 in octant `oct` (it made the
+// last arrival on the node's counter): reduce the node's <= 32 children
+// (adjacent-pair warp tree), publish it, arrive at the parent, and so on up
+// to the octant root; the warp completing the rank's last octant reduces the
+// rank root (and, in a single-rank job, finalizes v_{k+1} / the stop test).
+// Arrivals are acq_rel device-scope counters -- no spin-waits anywhere.
+// Lane 0 writes every node it publishes, so its acq_rel update orders exactly
+// the stores it covers.
+__device__ __forceinline__ void climb(const PassArgs& a, int oct, int l, int node, double* root_smem,
+                                      bool prologue) {
+  const int lane = threadIdx.x & 31;
+  const int nf = 2 * a.c + 2;
+  const Geometry& g = a.g;
+  const int loct = oct - g.oct0;
+  unsigned prev = 0;
+  for (;;) {
+    if (lane == 0) a.node_cnt[l][(int64_t)loct * g.nodes[l] + node] = 0u;
+    const int child = node * kFan + lane;
+    const bool real = child < octant_real_nodes(g, oct, l - 1);
+    const double* src = l == 1 ? a.tile_part + ((int64_t)oct * g.M - g.tile0 + child) * nf
+                               : a.node_part[l - 1] + ((int64_t)loct * g.nodes[l - 1] + child) * nf;
+    double* dst = a.node_part[l] + ((int64_t)loct * g.nodes[l] + node) * nf;
+    for (int f = 0; f < nf; ++f) {
+      double v = real ? __ldcg(src + f) : 0.0;
+      if (real) const_cast<double*>(src)[f] = sentinel();  // consumed: back to unpublished
+      v = warp_tree(v, f == nf - 1);
+      if (lane == 0) dst[f] = v;
+    }
+    if (l == g.levels) break;
+    node >>= 5;
+    ++l;
+    if (lane == 0) prev = atom_add_acq_rel(&a.node_cnt[l][(int64_t)loct * g.nodes[l] + node], 1u);
+    prev = __shfl_sync(0xffffffffu, prev, 0);
+    if ((int)prev != node_real_children(g, oct, l, node) - 1) return;
+  }
+  // octant root published: arrive at the rank
+  if (lane == 0) prev = atom_add_acq_rel(&a.ctl->rank_cnt, 1u);
+  prev = __shfl_sync(0xffffffffu, prev, 0);
+  if ((int)prev != rank_real_octants(g) - 1) return;
+  if (lane == 0) a.ctl->rank_cnt = 0u;
+  {
+    const bool real = lane < g.noct && (int64_t)(g.oct0 + lane) * g.M < g.T;
+    double* oroot = a.node_part[g.levels];  // one node per octant at the top level
+    for (int f = 0; f < nf; ++f) {
+      double v = real ? __ldcg(&oroot[lane * nf + f]) : 0.0;
+      if (real) oroot[lane * nf + f] = sentinel();
+      v = warp_tree(v, f == nf - 1);
+      if (lane == 0) {
+        a.rank_root[f] = v;
+        root_smem[f] = v;
+      }
+    }
+  }
+  __syncwarp();
+  if (lane == 0) {
+    if (a.finalize_local) finalize(a.ctl, root_smem, a.c, a.eps, a.max_iters, a.trace, prologue, a.cond, a.use_cond);
+    __threadfence();
+  }
+}
+
+// Octant / level-1 node of local tile lt.
+__device__ __forceinline__ void tile_node(const Geometry& g, int lt, int& oct, int& node) {
+  const int gt = g.tile0 + lt;
+  oct = gt / g.M;
+  node = (gt - oct * g.M) >> 5;
+}
+
+// One warp publishes the partial of local tile lt (part[f], shared memory),
+// arrives at its level-1 node and climbs when it completes it.
+__device__ __forceinline__ void publish_climb(const PassArgs& a, int lt, const double* part, double* root_smem,
+                                              bool prologue) {
+  const int lane = threadIdx.x & 31;
+  const int nf = 2 * a.c + 2;
+  if (lane == 0)
+    for (int f = 0; f < nf; ++f) a.tile_part[(int64_t)lt * nf + f] = part[f];
+  int oct, node;
+  tile_node(a.g, lt, oct, node);
+  unsigned prev = 0;
+  if (lane == 0) prev = atom_add_acq_rel(&a.node_cnt[1][(int64_t)(oct - a.g.oct0) * a.g.nodes[1] + node], 1u);
+  prev = __shfl_sync(0xffffffffu, prev, 0);
+  if ((int)prev != node_real_children(a.g, oct, 1, node) - 1) return;
+  climb(a, oct, 1, node, root_smem, prologue);
+}
+
+// Whole-CTA version (prologue and register-staged pass kernels): reduce the
+// per-thread payload of local tile lt to the tile partial, then warp 0
+// publishes and climbs while the other warps return to the stream; `buf`
+// double-buffers the per-warp scratch for that reason.
 template <int C, bool NAMED = false, typename SM>
 __device__ __forceinline__ void tile_finish(const PassArgs& a, int lt, const double* acc, SM& sm,
                                             bool prologue, int buf = 0) {
   constexpr int NS = 2 * C + 2;
   const int c = C <= 8 ? C : a.c, nf = 2 * c + 2;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const Geometry& g = a.g;
-
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int s = 0; s < NS; ++s) {
     double r = warp_tree(acc[s], s == NS - 1);
@@ -141,80 +248,16 @@ __device__ __forceinline__ void tile_finish(const PassArgs& a, int lt, const dou
   }
   red_sync<NAMED>();
   if (warp != 0) return;
-
-  // tile partial: adjacent-pair tree over the 8 warps, field per lane
-  double part = 0.0;
-  if (lane < nf) {
-    const bool mx = lane == nf - 1;
-    const double q0 = combine(sm.w[buf][0][lane], sm.w[buf][1][lane], mx);
-    const double q1 = combine(sm.w[buf][2][lane], sm.w[buf][3][lane], mx);
-    const double q2 = combine(sm.w[buf][4][lane], sm.w[buf][5][lane], mx);
-    const double q3 = combine(sm.w[buf][6][lane], sm.w[buf][7][lane], mx);
-    part = combine(combine(q0, q1, mx), combine(q2, q3, mx), mx);
-  }
-  for (int f = 0; f < nf; ++f) {
-    const double v = __shfl_sync(0xffffffffu, part, f);
-    if (lane == 0) a.tile_part[(int64_t)lt * nf + f] = v;
-  }
-
-  const int gt = g.tile0 + lt;
-  const int oct = gt / g.M;
-  const int grp = (gt - oct * g.M) / kGroup;
-  const int loct = oct - g.oct0;
-  const int lgrp = loct * g.gpo + grp;
-  unsigned prev = 0;
-  if (lane == 0) prev = atom_add_acq_rel(&a.group_cnt[lgrp], 1u);
-  prev = __shfl_sync(0xffffffffu, prev, 0);
-  if ((int)prev != group_real_tiles(g, oct, grp) - 1) return;
-
-  // last tile of the group: reduce the group's 32 leaves
-  if (lane == 0) a.group_cnt[lgrp] = 0u;
-  {
-    const int leaf = grp * kGroup + lane;
-    const bool real = leaf < g.M && (int64_t)oct * g.M + leaf < g.T;
-    const int64_t lt_leaf = (int64_t)oct * g.M + leaf - g.tile0;
-    for (int f = 0; f < nf; ++f) {
-      double v = real ? __ldcg(&a.tile_part[lt_leaf * nf + f]) : 0.0;
-      v = warp_tree(v, f == nf - 1);
-      if (lane == 0) a.group_root[(int64_t)lgrp * nf + f] = v;
-    }
-  }
-  if (lane == 0) prev = atom_add_acq_rel(&a.oct_cnt[loct], 1u);
-  prev = __shfl_sync(0xffffffffu, prev, 0);
-  if ((int)prev != octant_real_groups(g, oct) - 1) return;
-
-  // last group of the octant
-  if (lane == 0) a.oct_cnt[loct] = 0u;
-  {
-    const bool real = lane < g.gpo && group_real_tiles(g, oct, lane) > 0;
-    for (int f = 0; f < nf; ++f) {
-      double v = real ? __ldcg(&a.group_root[((int64_t)loct * g.gpo + lane) * nf + f]) : 0.0;
-      v = warp_tree(v, f == nf - 1);
-      if (lane == 0) a.oct_root[loct * nf + f] = v;
-    }
-  }
-  if (lane == 0) prev = atom_add_acq_rel(&a.ctl->rank_cnt, 1u);
-  prev = __shfl_sync(0xffffffffu, prev, 0);
-  if ((int)prev != rank_real_octants(g) - 1) return;
-
-  // last octant of the rank: the rank root (and, alone, the finalize)
-  if (lane == 0) a.ctl->rank_cnt = 0u;
-  {
-    const bool real = lane < g.noct && (int64_t)(g.oct0 + lane) * g.M < g.T;
-    for (int f = 0; f < nf; ++f) {
-      double v = real ? __ldcg(&a.oct_root[lane * nf + f]) : 0.0;
-      v = warp_tree(v, f == nf - 1);
-      if (lane == 0) {
-        a.rank_root[f] = v;
-        sm.root[f] = v;
-      }
-    }
+  for (int f = lane; f < nf; f += 32) {  // nf <= 34
+    const bool mx = f == nf - 1;
+    const double q0 = combine(sm.w[buf][0][f], sm.w[buf][1][f], mx);
+    const double q1 = combine(sm.w[buf][2][f], sm.w[buf][3][f], mx);
+    const double q2 = combine(sm.w[buf][4][f], sm.w[buf][5][f], mx);
+    const double q3 = combine(sm.w[buf][6][f], sm.w[buf][7][f], mx);
+    sm.part[f] = combine(combine(q0, q1, mx), combine(q2, q3, mx), mx);
   }
   __syncwarp();
-  if (lane == 0) {
-    if (a.finalize_local) finalize(a.ctl, sm.root, c, a.eps, a.max_iters, a.trace, prologue, a.cond, a.use_cond);
-    __threadfence();
-  }
+  publish_climb(a, lt, sm.part, sm.root, prologue);
 }
 
 // ---------------------------------------------------------------- loads ---
@@ -272,8 +315,8 @@ __device__ __forceinline__ void pass_tile(const PassArgs& a, int lt, const doubl
   const int c = a.c;
   const int64_t base = (int64_t)lt << a.g.tile_shift;
   const int steps = (1 << a.g.tile_shift) / (kThreads * kVec);
-  const float* __restrict__ ucur = a.u_cur;
-  float* __restrict__ unxt = a.u_nxt;
+  const float* ucur = a.u_cur;  // may alias unxt (in-place update)
+  float* unxt = a.u_nxt;
   const int64_t plane = a.g.plane;
 #pragma unroll 1
   for (int r = 0; r < steps; ++r) {
@@ -477,6 +520,22 @@ cudaError_t launch_pass_c(int xkind, int mode, const PassArgs& a, int sms, cudaS
 }
 
 template <int C>
+cudaError_t launch_loop_c(int xkind, int mode, const PassArgs& a, int sms, cudaStream_t st, int* grid_out,
+                          int variant, int force_grid) {
+  constexpr int MD = C <= 8 ? MODE_M2 : MODE_GEN;
+  const bool m2 = (mode == MODE_M2) && C <= 8;
+  if (variant == 1) return cudaErrorNotSupported;  // the LDG kernel has no loop form
+  if (xkind == XK_U8) {
+    if (C <= 8 && variant != 3 && (variant == 2 || !m2))
+      return launch_loop_tma<uint8_t, C, (C <= 8 ? MODE_LUT : MODE_GEN)>(a, sms, st, grid_out, force_grid);
+    return m2 ? launch_loop_tma<uint8_t, C, MD>(a, sms, st, grid_out, force_grid)
+              : launch_loop_tma<uint8_t, C, MODE_GEN>(a, sms, st, grid_out, force_grid);
+  }
+  return m2 ? launch_loop_tma<double, C, MD>(a, sms, st, grid_out, force_grid)
+            : launch_loop_tma<double, C, MODE_GEN>(a, sms, st, grid_out, force_grid);
+}
+
+template <int C>
 cudaError_t launch_prologue_c(int xkind, int mode, bool from_seed, const PassArgs& a, int sms,
                               cudaStream_t st) {
   auto go = [&](auto k) { k<<<occupancy_grid(k, a.g.tiles_local, sms), kThreads, 0, st>>>(a); };
@@ -510,6 +569,7 @@ cudaError_t launch_epilogue_c(int xkind, int mode, const EpilogueArgs& a, int sm
 
 #define FCM_INSTANTIATE(C)                                                                        \
   template cudaError_t launch_pass_c<C>(int, int, const PassArgs&, int, cudaStream_t, int*, int, int); \
+  template cudaError_t launch_loop_c<C>(int, int, const PassArgs&, int, cudaStream_t, int*, int, int); \
   template cudaError_t launch_prologue_c<C>(int, int, bool, const PassArgs&, int, cudaStream_t); \
   template cudaError_t launch_epilogue_c<C>(int, int, const EpilogueArgs&, int, cudaStream_t);
 

@@ -13,7 +13,7 @@ enum { XK_U8 = 0, XK_F64 = 2 };
 struct PassArgs {
   const void* x;          // pixels of this rank, padded to the plane length
   const float* u_cur;     // u_{k-1}, fp32 SoA: plane j at u_cur + j * plane
-  float* u_nxt;           // u_k
+  float* u_nxt;           // u_k (== u_cur: updated in place)
   const double* u0_aos;   // prologue source when not seeded
   uint64_t seed;          // prologue source when seeded
   int c;
@@ -23,18 +23,21 @@ struct PassArgs {
   int max_iters;
   int seq;                // pass sequence number in this run (tile-scheduler parity)
   Geometry g;
-  double* tile_part;      // [tiles_local][nf]
-  double* group_root;     // [noct * gpo][nf]
-  double* oct_root;       // [noct][nf]
+  double* tile_part;      // level 0: [tiles_local][nf]
+  double* node_part[kMaxLevels + 1];  // level l >= 1: [noct][nodes[l]][nf]
+  unsigned* node_cnt[kMaxLevels + 1]; // level l >= 1: [noct][nodes[l]] arrival counters
   double* rank_root;      // [nf]
-  unsigned* group_cnt;    // [noct * gpo]
-  unsigned* oct_cnt;      // [noct]
   Control* ctl;
   double* trace;          // [max_iters]
   cudaGraphConditionalHandle cond;  // device-side loop: while(cond) { pass } (graph mode)
   int use_cond;
   int finalize_local;     // 1: the CTA completing the rank root finalizes (single-rank jobs)
+  int keep_l2;            // 1: x + u fit in L2 -> evict_last loads/stores (next pass hits L2)
+  double* l1_buf;         // loop kernel: level-1 node results [2][noct][nodes[1]][nf] (pass parity)
+  uint64_t* prof;         // loop-kernel timeline [prof_passes][grid][kProbeSlots] or null
+  int prof_passes;
 };
+constexpr int kProbeSlots = 16;
 
 struct FinalizeArgs {
   const double* roots[kOctants];  // rank r's reduction root (peer, local or NCCL-gathered)
@@ -61,6 +64,10 @@ struct EpilogueArgs {
 
 // variant 0: TMA bulk-copy pipeline (default); 1: register-staged LDG kernel.
 cudaError_t launch_pass(int xkind, int c, int mode, const PassArgs& a, int sms, cudaStream_t st,
+                        int* grid_out, int variant = 0, int force_grid = 0);
+// Persistent loop kernel (all passes of a run in one cooperative launch);
+// returns cudaErrorCooperativeLaunchTooLarge when the grid cannot be resident.
+cudaError_t launch_loop(int xkind, int c, int mode, const PassArgs& a, int sms, cudaStream_t st,
                         int* grid_out, int variant = 0, int force_grid = 0);
 cudaError_t launch_prologue(int xkind, int c, int mode, bool from_seed, const PassArgs& a, int sms,
                             cudaStream_t st);

@@ -1,21 +1,42 @@
 // fcm_pass_tma.cuh -- the production FCM pass: TMA bulk-copy pipeline.
 //
-// One CTA = 8 consumer warps + 1 producer warp.  The producer claims tiles
-// from the dynamic scheduler and streams each 1024-voxel chunk of x and of
-// the c planes of u_{k-1} into a ring of shared-memory stages with
-// cp.async.bulk (TMA, completion counted on an mbarrier).  Consumers wait on
-// the stage's full barrier, evaluate Eq. 4 for 4 voxels per thread, store
-// u_k with 128-bit STG, fold the Eq. 3 / objective / delta terms into fp64
-// registers, release the stage, and at the end of each tile run the fixed
-// reduction tree (tile_finish).  Bytes in flight per SM are set by the ring
-// depth, not by registers, which is what an HBM-bound stream needs.
+// One CTA = 8 consumer warps + 1 producer warp + 1 reducer warp.  The
+// producer claims tiles from the dynamic scheduler and streams each
+// 1024-voxel chunk of x and of the c planes of u_{k-1} into a ring of
+// shared-memory stages with cp.async.bulk (TMA, completion counted on an
+// mbarrier).  Consumers wait on the stage's full barrier, evaluate Eq. 4 for
+// 4 voxels per thread, store u_k with 128-bit STG and fold the Eq. 3 /
+// objective / delta terms into fp64 registers; at the end of each tile every
+// consumer warp reduces its lanes (warp tree) into a shared-memory slot and
+// moves on.  The reducer warp combines the 8 warp values of each slot (the
+// top of the tile's fixed binary tree), publishes the tile partial and climbs
+// the global tree -- the device-scope fences and L2 round trips of the tree
+// never stall a consumer.  Bytes in flight per SM are set by the ring depth,
+// not by registers, which is what an HBM-bound stream needs.
 #pragma once
+#include <climits>
+
 #include "fcm_kernels.cuh"
 
 namespace fcm {
 
 constexpr int kChunk = kThreads * kVec;  // voxels per stage (1024)
-constexpr int kTmaThreads = kThreads + 32;
+constexpr int kTmaThreads = kThreads + 64;  // consumers | producer warp | reducer warp
+constexpr int kProducerTid = kThreads;
+constexpr int kReducerWarp = kThreads / 32 + 1;
+constexpr int kSlots = 8;  // tile-partial slots between consumers and the reducer (<= 32)
+
+// Consumer -> reducer handoff: per slot, the 8 warp-tree values of every
+// field of one tile (tile = -1: end of pass).  full: 8 warp arrivals;
+// empty: 1 reducer arrival.
+template <int NF>
+struct RedSlots {
+  double w[kSlots][kWarps][NF];
+  int tile[kSlots];
+  double root[NF];
+  uint64_t full[kSlots];
+  uint64_t empty[kSlots];
+};
 constexpr int kStageBudget = 100 * 1024;  // smem bytes of ring per CTA
 
 // ------------------------------------------------------------- PTX glue ---
@@ -34,6 +55,17 @@ __device__ __forceinline__ void mbar_arrive_tx(uint32_t bar, uint32_t bytes) {
 }
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
 }
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   asm volatile(
@@ -191,132 +223,207 @@ struct StageMeta {
   int pad;
 };
 
-template <typename XT, int C, int MODE>
-__global__ void __launch_bounds__(kTmaThreads, 2) pass_tma_kernel(PassArgs a) {
-  constexpr bool LUT = MODE == MODE_LUT;
+// Pipeline position of one role (producer or consumers).  Both sides walk
+// the ring in the same order, including the end-of-pass marker stage, so the
+// persistent loop kernel can run pass after pass on the same ring.
+struct Pipe {
+  int stage = 0;
+  uint32_t phase = 0;
+  template <int S>
+  __device__ __forceinline__ void advance() {
+    if (++stage == S) {
+      stage = 0;
+      phase ^= 1u;
+    }
+  }
+};
+
+// L2 residency: when x and the c membership planes fit in L2 (BrainWeb-sized
+// volumes, SURVEY config 2), loads and stores carry an evict_last policy so
+// the next pass -- the next iteration of the loop kernel -- hits L2 instead
+// of HBM.  Larger volumes stream with evict-first stores.
+__device__ __forceinline__ uint64_t l2_keep_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void bulk_g2s_keep(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar,
+                                              uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], "
+      "%4;" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void st_u4(float4* p, float4 v, bool keep, uint64_t pol) {
+  if (keep)
+    asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "f"(v.x), "f"(v.y),
+                 "f"(v.z), "f"(v.w), "l"(pol)
+                 : "memory");
+  else
+    __stcs(p, v);
+}
+// Orders this thread's generic-proxy view (u_k written by other CTAs, made
+// visible by the grid barrier) before its following TMA (async-proxy) reads.
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Optional per-CTA timeline of the loop kernel (FCM_OPT_PROFILE): slot k of
+// record (pass, CTA) -- 0 pass start, 1 producer done claiming, 2 consumers
+// done, 3 barrier released, 4 tiles claimed.
+__device__ __forceinline__ void probe(const PassArgs& a, unsigned it, int k, uint64_t v) {
+  if (a.prof && it <= (unsigned)a.prof_passes)
+    a.prof[((uint64_t)(it - 1) * gridDim.x + blockIdx.x) * kProbeSlots + k] = v;
+}
+
+// ------------------------------------------------------------ producer ----
+// One elected thread: claim tiles from `counter` until the rank's tiles are
+// exhausted, stream every chunk of x and of the c planes of u_{k-1} into the
+// ring, then post the end-of-pass marker.
+template <typename XT, int C, bool LUT>
+__device__ __forceinline__ int tma_produce(const PassArgs& a, uint8_t* smem, Pipe& ps, unsigned* counter,
+                                           unsigned it = 0) {
   using L = TmaLayout<XT, C, LUT>;
   constexpr int S = L::kStages;
-  extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ SmemRedT<2 * C + 2> sm;
-  if (pass_done(a, sm)) return;
-
-  const int tid = threadIdx.x;
   const uint32_t bar0 = smem_u32(smem + L::kBarOff);
-  auto full_bar = [&](int s) { return bar0 + 8u * s; };
-  auto empty_bar = [&](int s) { return bar0 + 8u * (S + s); };
   StageMeta* meta = reinterpret_cast<StageMeta*>(smem + L::kMetaOff);
-
-  if (tid == 0) {
-    for (int s = 0; s < S; ++s) {
-      mbar_init(full_bar(s), 1);
-      mbar_init(empty_bar(s), kWarps);
-    }
-    mbar_fence_init();
-    if (blockIdx.x == 0) a.ctl->tile_next[(a.seq + 1) & 1] = 0u;
-  }
-  __syncthreads();
-
   const int64_t tile = int64_t(1) << a.g.tile_shift;
   const int chunks_per_tile = (int)(tile / kChunk);
   const int c = C <= 8 ? C : a.c;
-
-  if (tid >= kThreads) {
-    // ---------------------------------------------------------- producer --
-    if (tid == kThreads) {
-      int stage = 0;
-      uint32_t phase = 0;
-      const int ntiles = a.g.tiles_local;
-      for (;;) {
-        const int lt = (int)atomicAdd(&a.ctl->tile_next[a.seq & 1], 1u);
-        if (lt >= ntiles) {
-          mbar_wait(empty_bar(stage), phase ^ 1u);
-          meta[stage].tile = -1;
-          mbar_arrive(full_bar(stage));
-          break;
-        }
-        const int64_t base = (int64_t)lt * tile;
-        const int64_t left = a.g.n_local - base;
-        const int64_t nch64 = (left + kChunk - 1) / kChunk;
-        const int nch = nch64 < chunks_per_tile ? (int)nch64 : chunks_per_tile;
-        for (int ch = 0; ch < nch; ++ch) {
-          mbar_wait(empty_bar(stage), phase ^ 1u);
-          meta[stage].tile = lt;
-          meta[stage].chunk = ch;
-          meta[stage].last = ch == nch - 1;
-          const uint32_t fb = full_bar(stage);
-          mbar_arrive_tx(fb, (uint32_t)(L::kXBytes + c * L::kUBytes));
-          const int64_t i0 = base + (int64_t)ch * kChunk;
-          uint8_t* st = smem + stage * L::kStageBytes;
-          bulk_g2s(smem_u32(st), reinterpret_cast<const XT*>(a.x) + i0, L::kXBytes, fb);
-#pragma unroll
-          for (int j = 0; j < C; ++j)
-            if (j < c)
-              bulk_g2s(smem_u32(st + L::kXBytes + j * L::kUBytes), a.u_cur + j * a.g.plane + i0,
-                       L::kUBytes, fb);
-          if (++stage == S) {
-            stage = 0;
-            phase ^= 1u;
-          }
-        }
-      }
+  const bool keep = a.keep_l2 != 0;
+  const uint64_t pol = keep ? l2_keep_policy() : 0ull;
+  const int ntiles = a.g.tiles_local;
+  int claimed = 0;
+  for (;;) {
+    const int lt = (int)atomicAdd(counter, 1u);
+    if (lt >= ntiles) {
+      mbar_wait(bar0 + 8u * (S + ps.stage), ps.phase ^ 1u);
+      meta[ps.stage].tile = -1;
+      mbar_arrive(bar0 + 8u * ps.stage);
+      ps.advance<S>();
+      return claimed;
     }
-    return;
-  }
-
-  // ------------------------------------------------------------ consumers --
-  double v[C];
+    ++claimed;
+    if (it) probe(a, it, 5, global_ns());
+    const int64_t base = (int64_t)lt * tile;
+    const int64_t left = a.g.n_local - base;
+    const int64_t nch64 = (left + kChunk - 1) / kChunk;
+    const int nch = nch64 < chunks_per_tile ? (int)nch64 : chunks_per_tile;
+    for (int ch = 0; ch < nch; ++ch) {
+      mbar_wait(bar0 + 8u * (S + ps.stage), ps.phase ^ 1u);
+      meta[ps.stage].tile = lt;
+      meta[ps.stage].chunk = ch;
+      meta[ps.stage].last = ch == nch - 1;
+      const uint32_t fb = bar0 + 8u * ps.stage;
+      mbar_arrive_tx(fb, (uint32_t)(L::kXBytes + c * L::kUBytes));
+      const int64_t i0 = base + (int64_t)ch * kChunk;
+      uint8_t* st = smem + ps.stage * L::kStageBytes;
+      const void* xs = reinterpret_cast<const XT*>(a.x) + i0;
+      if (keep) bulk_g2s_keep(smem_u32(st), xs, L::kXBytes, fb, pol);
+      else bulk_g2s(smem_u32(st), xs, L::kXBytes, fb);
 #pragma unroll
-  for (int j = 0; j < C; ++j) v[j] = j < c ? a.ctl->v[j] : 0.0;
-  const Powers pw = load_powers(a);
+      for (int j = 0; j < C; ++j)
+        if (j < c) {
+          const uint32_t dst = smem_u32(st + L::kXBytes + j * L::kUBytes);
+          const float* src = a.u_cur + j * a.g.plane + i0;
+          if (keep) bulk_g2s_keep(dst, src, L::kUBytes, fb, pol);
+          else bulk_g2s(dst, src, L::kUBytes, fb);
+        }
+      ps.advance<S>();
+    }
+  }
+}
+
+// ------------------------------------------------------- intensity table --
+// Entry b = tid: the same robust Eq. 4 evaluation as the direct path, so
+// table values equal per-voxel evaluation.  Ends with a consumer barrier.
+template <int C>
+__device__ __forceinline__ void tma_build_lut(uint8_t* lut, const double* v, int c, const Powers& pw) {
   using LL = LutLayout<C>;
-  uint8_t* lut = smem + L::kLutOff;
-  if (LUT) {
-    // entry b = tid: the same robust Eq. 4 evaluation as the direct path
-    const double xb = (double)tid;
-    double u[C];
-    membership<C, MODE_GEN>(xb, v, c, pw, u);
-    double jt = 0.0;
-    float ufv[4 * LL::K4], duv[4 * LL::K4];
-    double wv[2 * LL::K2];
+  const int tid = threadIdx.x;
+  const double xb = (double)tid;
+  double u[C];
+  membership<C, MODE_GEN>(xb, v, c, pw, u);
+  double jt = 0.0;
+  float ufv[4 * LL::K4], duv[4 * LL::K4];
+  double wv[2 * LL::K2];
 #pragma unroll
-    for (int j = 0; j < 4 * LL::K4; ++j) ufv[j] = duv[j] = 0.0f;
+  for (int j = 0; j < 4 * LL::K4; ++j) ufv[j] = duv[j] = 0.0f;
 #pragma unroll
-    for (int j = 0; j < 2 * LL::K2; ++j) wv[j] = 0.0;
+  for (int j = 0; j < 2 * LL::K2; ++j) wv[j] = 0.0;
 #pragma unroll
-    for (int j = 0; j < C; ++j) {
-      const double w = pow_m<MODE_GEN>(u[j], pw);
-      const double d = xb - v[j];
-      jt = fma(w, d * d, jt);
-      wv[j] = w;
-      ufv[j] = (float)u[j];
-      duv[j] = (float)(u[j] - (double)ufv[j]);
-    }
-#pragma unroll
-    for (int k = 0; k < LL::K4; ++k) {
-      reinterpret_cast<float4*>(lut + LL::kUfOff)[k * 256 + tid] =
-          make_float4(ufv[4 * k], ufv[4 * k + 1], ufv[4 * k + 2], ufv[4 * k + 3]);
-      reinterpret_cast<float4*>(lut + LL::kDuOff)[k * 256 + tid] =
-          make_float4(duv[4 * k], duv[4 * k + 1], duv[4 * k + 2], duv[4 * k + 3]);
-    }
-#pragma unroll
-    for (int k = 0; k < LL::K2; ++k)
-      reinterpret_cast<double2*>(lut + LL::kWOff)[k * 256 + tid] = make_double2(wv[2 * k], wv[2 * k + 1]);
-    reinterpret_cast<double*>(lut + LL::kJOff)[tid] = jt;
-    red_sync<true>();
+  for (int j = 0; j < C; ++j) {
+    const double w = pow_m<MODE_GEN>(u[j], pw);
+    const double d = xb - v[j];
+    jt = fma(w, d * d, jt);
+    wv[j] = w;
+    ufv[j] = (float)u[j];
+    duv[j] = (float)(u[j] - (double)ufv[j]);
   }
+#pragma unroll
+  for (int k = 0; k < LL::K4; ++k) {
+    reinterpret_cast<float4*>(lut + LL::kUfOff)[k * 256 + tid] =
+        make_float4(ufv[4 * k], ufv[4 * k + 1], ufv[4 * k + 2], ufv[4 * k + 3]);
+    reinterpret_cast<float4*>(lut + LL::kDuOff)[k * 256 + tid] =
+        make_float4(duv[4 * k], duv[4 * k + 1], duv[4 * k + 2], duv[4 * k + 3]);
+  }
+#pragma unroll
+  for (int k = 0; k < LL::K2; ++k)
+    reinterpret_cast<double2*>(lut + LL::kWOff)[k * 256 + tid] = make_double2(wv[2 * k], wv[2 * k + 1]);
+  reinterpret_cast<double*>(lut + LL::kJOff)[tid] = jt;
+  red_sync<true>();
+}
+
+// ------------------------------------------------------------ consumers ---
+// The 8 consumer warps: per stage, copy 4 voxels per thread to registers,
+// release the stage, evaluate Eq. 4, store u_k (in place over u_{k-1}: each
+// element is in the stage before the same thread overwrites it) and fold the
+// Eq. 3 / objective / delta terms; at the end of each tile run the fixed
+// reduction tree.  Returns after the end-of-pass marker.
+template <typename XT, int C, int MODE>
+__device__ __forceinline__ void tma_consume(const PassArgs& a, uint8_t* smem, Pipe& ps,
+                                            RedSlots<2 * C + 2>& rs, Pipe& sp, const double* v,
+                                            const Powers& pw) {
+  constexpr bool LUT = MODE == MODE_LUT;
+  using L = TmaLayout<XT, C, LUT>;
+  using LL = LutLayout<C>;
+  constexpr int S = L::kStages;
+  const int tid = threadIdx.x;
+  const uint32_t bar0 = smem_u32(smem + L::kBarOff);
+  const StageMeta* meta = reinterpret_cast<const StageMeta*>(smem + L::kMetaOff);
+  const uint8_t* lut = smem + L::kLutOff;
+  const int64_t tile = int64_t(1) << a.g.tile_shift;
+  const int c = C <= 8 ? C : a.c;
+  const bool keep = a.keep_l2 != 0;
+  const uint64_t pol = keep ? l2_keep_policy() : 0ull;
   float dmax_f = 0.0f;
-  int tile_parity = 0;
   double acc[2 * C + 2];
 #pragma unroll
   for (int s = 0; s < 2 * C + 2; ++s) acc[s] = 0.0;
   uint32_t dmax_hi = 0;
-  int stage = 0;
-  uint32_t phase = 0;
   for (;;) {
-    mbar_wait(full_bar(stage), phase);
-    const StageMeta mt = meta[stage];
-    if (mt.tile < 0) break;
-    const uint8_t* st = smem + stage * L::kStageBytes;
+    mbar_wait(bar0 + 8u * ps.stage, ps.phase);
+    const StageMeta mt = meta[ps.stage];
+    const uint8_t* st = smem + ps.stage * L::kStageBytes;
+    if (mt.tile < 0) {
+      __syncwarp();
+      if ((tid & 31) == 0) mbar_arrive(bar0 + 8u * (S + ps.stage));
+      ps.advance<S>();
+      // end-of-pass slot for the reducer
+      mbar_wait(smem_u32(&rs.empty[sp.stage]), sp.phase ^ 1u);
+      if (tid == 0) rs.tile[sp.stage] = -1;
+      __syncwarp();
+      if ((tid & 31) == 0) mbar_arrive(smem_u32(&rs.full[sp.stage]));
+      sp.advance<kSlots>();
+      return;
+    }
     const int64_t i0 = (int64_t)mt.tile * tile + (int64_t)mt.chunk * kChunk + tid * kVec;
     const int64_t nleft = a.g.n_local - i0;
     double xd[4];
@@ -337,11 +444,8 @@ __global__ void __launch_bounds__(kTmaThreads, 2) pass_tma_kernel(PassArgs a) {
     for (int j = 0; j < C; ++j)
       if (j < c) uo[j] = *reinterpret_cast<const float4*>(st + L::kXBytes + j * L::kUBytes + tid * 16);
     __syncwarp();
-    if ((tid & 31) == 0) mbar_arrive(empty_bar(stage));
-    if (++stage == S) {
-      stage = 0;
-      phase ^= 1u;
-    }
+    if ((tid & 31) == 0) mbar_arrive(bar0 + 8u * (S + ps.stage));
+    ps.advance<S>();
     float4 un[C];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -387,16 +491,488 @@ __global__ void __launch_bounds__(kTmaThreads, 2) pass_tma_kernel(PassArgs a) {
     }
 #pragma unroll
     for (int j = 0; j < C; ++j)
-      if (j < c) __stcs(reinterpret_cast<float4*>(a.u_nxt + j * a.g.plane + i0), un[j]);
+      if (j < c) st_u4(reinterpret_cast<float4*>(a.u_nxt + j * a.g.plane + i0), un[j], keep, pol);
     if (mt.last) {
       acc[2 * C + 1] = LUT ? (double)dmax_f : __hiloint2double((int)dmax_hi, (int)0xffffffffu);
-      tile_finish<C, true>(a, mt.tile, acc, sm, false, tile_parity);
-      tile_parity ^= 1;
+      // lanes -> warp value per field (adjacent-pair tree), then hand the
+      // 8 warp values to the reducer through a slot
+      constexpr int NS = 2 * C + 2;
+      double r[NS];
+#pragma unroll
+      for (int s2 = 0; s2 < NS; ++s2) r[s2] = warp_tree(acc[s2], s2 == NS - 1);
+      mbar_wait(smem_u32(&rs.empty[sp.stage]), sp.phase ^ 1u);
+      if ((tid & 31) == 0) {
+#pragma unroll
+        for (int s2 = 0; s2 < NS; ++s2) {
+          const int f = field_of<C>(s2, c);
+          if (f >= 0) rs.w[sp.stage][tid >> 5][f] = r[s2];
+        }
+        if (tid == 0) rs.tile[sp.stage] = mt.tile;
+      }
+      __syncwarp();
+      if ((tid & 31) == 0) mbar_arrive(smem_u32(&rs.full[sp.stage]));
+      sp.advance<kSlots>();
 #pragma unroll
       for (int s = 0; s < 2 * C + 2; ++s) acc[s] = 0.0;
       dmax_hi = 0;
       dmax_f = 0.0f;
     }
+  }
+}
+
+// ------------------------------------------------------------- reducer ----
+// Poll-and-reduce of one tree node by one warp: lane i reads child i's NF
+// fields (children < nreal; the rest count as 0.0).  Returns false, without
+// side effects, while any child is unpublished; otherwise resets the children
+// to unpublished and leaves the per-field adjacent-pair warp tree in lane 0
+// of out[f] (out in shared or global memory, written by lane 0).
+template <int NF, bool GLOBAL_OUT>
+__device__ __forceinline__ bool try_node(double* child0, int nreal, int nf, double* out) {
+  const int lane = threadIdx.x & 31;
+  const bool real = lane < nreal;
+  double* src = child0 + (int64_t)lane * nf;
+  bool ok = !real || !is_sentinel(ld_relaxed(src + nf - 1));
+  if (!__all_sync(0xffffffffu, ok)) return false;
+  double v[NF];
+#pragma unroll
+  for (int f = 0; f < NF; ++f) {
+    v[f] = 0.0;
+    if (f < nf && real) {
+      v[f] = ld_relaxed(src + f);
+      ok = ok && !is_sentinel(v[f]);
+    }
+  }
+  if (!__all_sync(0xffffffffu, ok)) return false;
+#pragma unroll
+  for (int f = 0; f < NF; ++f)
+    if (f < nf) {
+      if (real) st_relaxed(src + f, sentinel());
+      const double r = warp_tree(v[f], f == nf - 1);
+      if (lane == 0) {
+        if (GLOBAL_OUT) st_relaxed(out + f, r);
+        else out[f] = r;
+      }
+    }
+  return true;
+}
+
+template <int NF, bool GLOBAL_OUT>
+__device__ __forceinline__ void wait_node(double* child0, int nreal, int nf, double* out) {
+  while (!try_node<NF, GLOBAL_OUT>(child0, nreal, nf, out)) __nanosleep(128);
+}
+
+// Node k of CTA 0's upper-level list -- levels 2..L, octant by octant, each
+// octant's level-2 nodes before its level-3 node -- as (level, octant, j).
+__device__ __forceinline__ void upper_node(const Geometry& g, int k, int& l, int& lo, int& j) {
+  int per = 0;
+  for (int m = 2; m <= g.levels; ++m) per += g.nodes[m];
+  lo = k / per;
+  j = k - lo * per;
+  l = 2;
+  while (j >= g.nodes[l]) {
+    j -= g.nodes[l];
+    ++l;
+  }
+}
+
+// One warp per CTA.  It (1) drains the consumers' slots: per slot the 8-warp
+// pair tree per field (the top three levels of the tile's binary tree over
+// its 256 threads) and a relaxed publish of the tile partial -- no fence, no
+// atomic on the streaming path; (2) in the gaps, reduces the level-1 nodes
+// this CTA owns once the scheduler has handed out all their tiles and every
+// child is visibly published (fixed owners: no last-arriver races, no
+// feedback onto slow CTAs).
+//   LOOP (persistent kernel): level-1 node z belongs to CTA z mod G and its
+//     result goes to l1_out (plain stores; the grid barrier that follows
+//     publishes it, every CTA then reduces the levels above redundantly);
+//   per-pass kernels: node z belongs to CTA 1 + z mod (G-1), results are
+//     published with the sentinel protocol, and CTA 0 owns the levels above
+//     (octant by octant), the rank root and the finalize.
+template <int C, bool LOOP>
+__device__ __forceinline__ void tma_reduce(const PassArgs& a, RedSlots<2 * C + 2>& rs, Pipe& sp,
+                                           const unsigned* counter, double* l1_out, unsigned it = 0) {
+  constexpr int NF = 2 * C + 2;
+  const int lane = threadIdx.x & 31;
+  const int nf = 2 * a.c + 2;
+  const Geometry& g = a.g;
+  const int G = gridDim.x;
+  const bool cta0 = blockIdx.x == 0;
+  const int NA = g.noct * g.nodes[1];  // list A: level-1 nodes
+  int per = 0;
+  for (int m = 2; m <= g.levels; ++m) per += g.nodes[m];
+  const int NB = (!LOOP && cta0) ? g.noct * per : 0;  // list B: CTA 0's upper levels
+  int strideA, za;
+  if (LOOP || G == 1) {
+    strideA = G;
+    za = blockIdx.x;
+  } else {
+    strideA = G - 1;
+    za = cta0 ? NA : (int)blockIdx.x - 1;
+  }
+  int zb = 0;
+  bool slots_done = false;
+  uint64_t n_poll = 0, n_node = 0;
+  while (!slots_done || za < NA || zb < NB) {
+    if (!slots_done && mbar_test(smem_u32(&rs.full[sp.stage]), sp.phase)) {
+      const int t = rs.tile[sp.stage];
+      if (t >= 0) {
+        for (int f = lane; f < nf; f += 32) {  // nf <= 34
+          const bool mx = f == nf - 1;
+          const double(*w)[NF] = rs.w[sp.stage];
+          const double q0 = combine(w[0][f], w[1][f], mx);
+          const double q1 = combine(w[2][f], w[3][f], mx);
+          const double q2 = combine(w[4][f], w[5][f], mx);
+          const double q3 = combine(w[6][f], w[7][f], mx);
+          st_relaxed(a.tile_part + (int64_t)t * nf + f, combine(combine(q0, q1, mx), combine(q2, q3, mx), mx));
+        }
+      } else {
+        slots_done = true;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&rs.empty[sp.stage]));
+      sp.advance<kSlots>();
+      continue;
+    }
+    int l, lo, j;
+    if (za < NA) {
+      l = 1;
+      lo = za / g.nodes[1];
+      j = za - lo * g.nodes[1];
+    } else if (zb < NB) {
+      upper_node(g, zb, l, lo, j);
+    } else {
+      __nanosleep(64);
+      continue;
+    }
+    const int oct = g.oct0 + lo;
+    const int nreal = node_real_children(g, oct, l, j);
+    bool advance = nreal == 0;  // unreal node: nothing to do
+    if (!advance) {
+      // every tile under the node handed out?  (local index of its last tile)
+      const long long r0 = octant_real_nodes(g, oct, 0);
+      const long long last = min(((long long)j + 1) << (5 * l), r0) - 1;
+      const int last_lt = (int)((long long)oct * g.M - g.tile0 + last);
+      if ((int)ld_relaxed_u32(counter) > last_lt) {
+        ++n_poll;
+        double* child0 = l == 1 ? a.tile_part + ((int64_t)oct * g.M - g.tile0 + (int64_t)j * kFan) * nf
+                                : a.node_part[l - 1] + ((int64_t)lo * g.nodes[l - 1] + (int64_t)j * kFan) * nf;
+        if (LOOP)
+          advance = try_node<NF, false>(child0, nreal, nf, l1_out + ((int64_t)lo * g.nodes[1] + j) * nf);
+        else
+          advance = try_node<NF, true>(child0, nreal, nf, a.node_part[l] + ((int64_t)lo * g.nodes[l] + j) * nf);
+        n_node += advance;
+      }
+    }
+    if (advance) {
+      if (za < NA) za += strideA;
+      else ++zb;
+    } else {
+      __nanosleep(64);
+    }
+  }
+  if (!LOOP && cta0) {
+    // octant roots (one level-L node per octant; real octants are a prefix)
+    wait_node<NF, false>(a.node_part[g.levels], rank_real_octants(g), nf, rs.root);
+    __syncwarp();
+    for (int f = lane; f < nf; f += 32) a.rank_root[f] = rs.root[f];
+    __syncwarp();
+    if (lane == 0) {
+      if (a.finalize_local)
+        finalize(a.ctl, rs.root, a.c, a.eps, a.max_iters, a.trace, false, a.cond, a.use_cond);
+      __threadfence();
+    }
+  }
+  if (it && lane == 0) {
+    probe(a, it, 8, n_poll);
+    probe(a, it, 9, n_node);
+  }
+}
+
+// The adjacent-pair tree over 32 children (identical association to
+// warp_tree: ((c0+c1)+(c2+c3))+... up to (c0..15)+(c16..31)), evaluated by ONE
+// lane from memory (child i at p[i*stride]; children >= nreal count as 0.0):
+// no shuffles, so a warp evaluates up to 32 fields side by side.
+template <bool GLOBAL>
+__device__ __forceinline__ double tree8(const double* p, int64_t stride, int i0, int nreal, bool mx) {
+  double v[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+    v[i] = (i0 + i < nreal) ? (GLOBAL ? __ldcg(p + (int64_t)(i0 + i) * stride) : p[(int64_t)(i0 + i) * stride]) : 0.0;
+  return combine(combine(combine(v[0], v[1], mx), combine(v[2], v[3], mx), mx),
+                 combine(combine(v[4], v[5], mx), combine(v[6], v[7], mx), mx), mx);
+}
+template <bool GLOBAL>
+__device__ __forceinline__ double tree32(const double* p, int64_t stride, int nreal, bool mx) {
+  const double t0 = tree8<GLOBAL>(p, stride, 0, nreal, mx);
+  const double t1 = nreal > 8 ? tree8<GLOBAL>(p, stride, 8, nreal, mx) : 0.0;
+  const double t2 = nreal > 16 ? tree8<GLOBAL>(p, stride, 16, nreal, mx) : 0.0;
+  const double t3 = nreal > 24 ? tree8<GLOBAL>(p, stride, 24, nreal, mx) : 0.0;
+  return combine(combine(t0, t1, mx), combine(t2, t3, mx), mx);
+}
+
+// Loop kernel, after the grid barrier of pass `it`: every CTA reduces the
+// levels above 1 from the published level-1 results (l1, [noct][nodes[1]][nf]),
+// the same fixed tree as everywhere else, into root[] -- redundantly, so no
+// further cross-CTA hop is needed.  Lane = field (tree32), warps share the
+// nodes of a level.  All kTmaThreads threads call it; scratch is the (idle)
+// stage ring.
+template <int NF>
+__device__ __forceinline__ void loop_upper(const PassArgs& a, const double* l1, double* scratch,
+                                           double (*oroot)[NF], double* root) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int kW = kTmaThreads / 32;
+  const int nf = 2 * a.c + 2;
+  const Geometry& g = a.g;
+  const int per = g.levels == 3 ? g.nodes[2] : 1;
+  // step 1: level-2 nodes (L == 3) or octant roots (L == 2) from level-1 results
+  if (g.levels >= 2) {
+    for (int item = warp; item < g.noct * per; item += kW) {
+      const int lo = item / per, k = item - lo * per;
+      const int oct = g.oct0 + lo;
+      const int nreal = (int64_t)oct * g.M < g.T ? node_real_children(g, oct, 2, k) : 0;
+      const double* src = l1 + ((int64_t)lo * g.nodes[1] + (int64_t)k * kFan) * nf;
+      for (int f = lane; f < nf; f += 32)
+        scratch[(int64_t)item * NF + f] = nreal ? tree32<true>(src + f, nf, nreal, f == nf - 1) : 0.0;
+    }
+  }
+  __syncthreads();
+  // step 2: octant roots
+  for (int lo = warp; lo < g.noct; lo += kW) {
+    const int oct = g.oct0 + lo;
+    const bool oreal = (int64_t)oct * g.M < g.T;
+    for (int f = lane; f < nf; f += 32) {
+      double r = 0.0;
+      if (oreal) {
+        if (g.levels == 1) r = __ldcg(l1 + (int64_t)lo * nf + f);  // the level-1 node is the octant root
+        else if (g.levels == 2) r = scratch[(int64_t)lo * NF + f];
+        else r = tree32<false>(scratch + (int64_t)lo * per * NF + f, NF, (int)octant_real_nodes(g, oct, 2), f == nf - 1);
+      }
+      oroot[lo][f] = r;
+    }
+  }
+  __syncthreads();
+  // step 3: the rank root over the rank's octants
+  if (warp == 0) {
+    int nreal = 0;
+    for (int lo = 0; lo < g.noct; ++lo) nreal += ((int64_t)(g.oct0 + lo) * g.M < g.T) ? 1 : 0;
+    for (int f = lane; f < nf; f += 32) {
+      double v[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = i < nreal ? oroot[i][f] : 0.0;
+      const bool mx = f == nf - 1;
+      root[f] = combine(combine(combine(v[0], v[1], mx), combine(v[2], v[3], mx), mx),
+                        combine(combine(v[4], v[5], mx), combine(v[6], v[7], mx), mx), mx);
+    }
+  }
+  __syncthreads();
+}
+
+template <typename XT, int C, bool LUT>
+__device__ __forceinline__ void tma_init_barriers(uint8_t* smem, RedSlots<2 * C + 2>& rs) {
+  using L = TmaLayout<XT, C, LUT>;
+  const uint32_t bar0 = smem_u32(smem + L::kBarOff);
+  for (int s = 0; s < L::kStages; ++s) {
+    mbar_init(bar0 + 8u * s, 1);
+    mbar_init(bar0 + 8u * (L::kStages + s), kWarps);
+  }
+  for (int s = 0; s < kSlots; ++s) {
+    mbar_init(smem_u32(&rs.full[s]), kWarps);
+    mbar_init(smem_u32(&rs.empty[s]), 1);
+  }
+  mbar_fence_init();
+}
+
+template <int C>
+__device__ __forceinline__ void load_centers(const Control* ctl, int c, double* v) {
+#pragma unroll
+  for (int j = 0; j < C; ++j) v[j] = j < c ? __ldcg(&ctl->v[j]) : 0.0;
+}
+
+// ------------------------------------------------- one pass per launch ----
+template <typename XT, int C, int MODE>
+__global__ void __launch_bounds__(kTmaThreads, 2) pass_tma_kernel(PassArgs a) {
+  constexpr bool LUT = MODE == MODE_LUT;
+  using L = TmaLayout<XT, C, LUT>;
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ RedSlots<2 * C + 2> rs;
+  __shared__ int s_done;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    int done = *(volatile int*)&a.ctl->done;
+    if (blockIdx.x == 0 && a.seq != 0) {
+      const unsigned launched = a.ctl->launches++;
+      if (!done && a.use_cond && launched > (unsigned)a.max_iters + 8u) {
+        a.ctl->dead = -2;  // watchdog: a device loop may never outlive max_iters passes
+        a.ctl->done = 1;
+        done = 1;
+      }
+      if (done && a.use_cond) cudaGraphSetConditional(a.cond, 0u);
+    }
+    s_done = done;
+    if (!done) {
+      tma_init_barriers<XT, C, LUT>(smem, rs);
+      if (blockIdx.x == 0) a.ctl->tile_next[(a.seq + 1) & 1] = 0u;
+    }
+  }
+  __syncthreads();
+  if (s_done) return;
+  Pipe ps, sp;
+  if (tid >= kThreads) {
+    if (tid == kProducerTid) tma_produce<XT, C, LUT>(a, smem, ps, &a.ctl->tile_next[a.seq & 1]);
+    else if ((tid >> 5) == kReducerWarp)
+      tma_reduce<C, false>(a, rs, sp, &a.ctl->tile_next[a.seq & 1], nullptr);
+    return;
+  }
+  const int c = C <= 8 ? C : a.c;
+  double v[C];
+  load_centers<C>(a.ctl, c, v);
+  const Powers pw = load_powers(a);
+  if (LUT) tma_build_lut<C>(smem + L::kLutOff, v, c, pw);
+  tma_consume<XT, C, MODE>(a, smem, ps, rs, sp, v, pw);
+}
+
+// -------------------------------------------------------- grid barrier ----
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Called by thread 0 of every CTA after a CTA barrier that follows the CTA's
+// last tile of pass `it`.  The last arriver knows every tile of the pass is
+// finished (so the reduction root and its finalize are published) and every
+// producer has stopped claiming, so it re-arms the tile scheduler and
+// releases generation `it`.  A stuck barrier (which co-residency rules out)
+// times out after 4 s, flags the run, and lets every CTA leave.
+__device__ __forceinline__ bool grid_barrier(Control* ctl, unsigned it, unsigned ncta) {
+  __threadfence();
+  const unsigned prev = atomicAdd(&ctl->bar_count, 1u);
+  if (prev == it * ncta - 1u) {
+    ctl->tile_next[1] = 0u;
+    __threadfence();
+    st_release_u32(&ctl->epoch, it);
+    return true;
+  }
+  const uint64_t t0 = global_ns();
+  while (ld_acquire_u32(&ctl->epoch) < it) {
+    if (global_ns() - t0 > 4000000000ull) {
+      ctl->dead = -3;
+      ctl->done = 1;
+      __threadfence();
+      return false;
+    }
+  }
+  return true;
+}
+
+// Loop kernel, thread 0 of every CTA after the redundant root of pass `it`:
+// the same decisions as finalize_body (core.py:120-131: converged, max_iters,
+// DegenerateClusterError(j), else v_{k+1}) on the CTA's own copy; CTA 0 also
+// publishes them to the control block and the trace.
+__device__ __forceinline__ void finalize_loop(const PassArgs& a, const double* root, unsigned it, double* vsh,
+                                              int* s_done) {
+  const int c = a.c;
+  const int k = (int)it;
+  const double delta = root[2 * c + 1];
+  const bool conv = delta < a.eps;
+  bool done = conv || k >= a.max_iters;
+  int dead = -1;
+  if (!done)
+    for (int j = 0; j < c; ++j)
+      if (root[c + j] == 0.0) {
+        dead = j;
+        done = true;
+        break;
+      }
+  if (!done)
+    for (int j = 0; j < c; ++j) vsh[j] = root[j] / root[c + j];
+  *s_done = done ? 1 : 0;
+  if (blockIdx.x == 0) {
+    Control* ctl = a.ctl;
+    for (int f = 0; f < 2 * c + 2; ++f) {
+      ctl->root[f] = root[f];
+      a.rank_root[f] = root[f];
+    }
+    ctl->iter = k;
+    a.trace[k - 1] = root[2 * c];
+    ctl->delta = delta;
+    ctl->converged = conv ? 1 : 0;
+    ctl->dead = dead;
+    if (!done)
+      for (int j = 0; j < c; ++j) ctl->v[j] = vsh[j];
+    ctl->done = done ? 1 : 0;
+  }
+}
+
+// --------------------------------------------- persistent loop kernel -----
+// The whole device loop of core._iterate (core.py:118-131) in ONE launch:
+// every CTA stays resident (cooperative launch), runs pass after pass over
+// the dynamic tile scheduler, and meets the others at a grid barrier between
+// passes; the CTA that completes a pass's reduction tree finalizes v_{k+1}
+// and the stop test before it arrives.  u is updated in place.  No
+// per-iteration launch, no host round trip, ring barriers initialised once.
+template <typename XT, int C, int MODE>
+__global__ void __launch_bounds__(kTmaThreads, 2) loop_tma_kernel(PassArgs a) {
+  constexpr bool LUT = MODE == MODE_LUT;
+  constexpr int NF = 2 * C + 2;
+  using L = TmaLayout<XT, C, LUT>;
+  static_assert(L::kRingBytes >= kOctants * kFan * NF * 8, "ring too small for the upper-level scratch");
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ RedSlots<NF> rs;
+  __shared__ double oroot[kOctants][NF];
+  __shared__ double vsh[C];
+  __shared__ int s_done;
+  const int tid = threadIdx.x;
+  const int c = C <= 8 ? C : a.c;
+  if (tid == 0) {
+    tma_init_barriers<XT, C, LUT>(smem, rs);
+    s_done = *(volatile int*)&a.ctl->done;
+    for (int j = 0; j < c; ++j) vsh[j] = __ldcg(&a.ctl->v[j]);
+  }
+  const Powers pw = load_powers(a);
+  const int64_t l1_len = (int64_t)a.g.noct * a.g.nodes[1] * (2 * a.c + 2);
+  Pipe ps, sp;
+  __syncthreads();
+  for (unsigned it = 1; !s_done && it <= (unsigned)a.max_iters; ++it) {
+    if (tid == 0) probe(a, it, 0, global_ns());
+    double* l1 = a.l1_buf + (it & 1) * l1_len;  // parity: readers of pass it-1 may still read the other half
+    if (tid >= kThreads) {
+      if (tid == kProducerTid) {
+        fence_proxy_async_global();
+        const int n = tma_produce<XT, C, LUT>(a, smem, ps, &a.ctl->tile_next[1], it);  // zeroed by the prologue
+        probe(a, it, 1, global_ns());
+        probe(a, it, 4, (uint64_t)n);
+        unsigned smid;
+        asm("mov.u32 %0, %%smid;" : "=r"(smid));
+        probe(a, it, 6, smid);
+      } else if ((tid >> 5) == kReducerWarp) {
+        tma_reduce<C, true>(a, rs, sp, &a.ctl->tile_next[1], l1, it);
+        if ((tid & 31) == 0) probe(a, it, 7, global_ns());
+      }
+    } else {
+      double v[C];
+#pragma unroll
+      for (int j = 0; j < C; ++j) v[j] = j < c ? vsh[j] : 0.0;
+      if (LUT) tma_build_lut<C>(smem + L::kLutOff, v, c, pw);
+      tma_consume<XT, C, MODE>(a, smem, ps, rs, sp, v, pw);
+      if (tid == 0) probe(a, it, 2, global_ns());
+    }
+    __syncthreads();
+    if (tid == 0) {
+      if (!grid_barrier(a.ctl, it, gridDim.x)) s_done = 1;
+      probe(a, it, 3, global_ns());
+    }
+    __syncthreads();
+    if (s_done) break;
+    loop_upper<NF>(a, l1, reinterpret_cast<double*>(smem), oroot, rs.root);
+    if (tid == 0) {
+      finalize_loop(a, rs.root, it, vsh, &s_done);
+      probe(a, it, 14, global_ns());
+    }
+    __syncthreads();
   }
 }
 
@@ -422,6 +998,38 @@ inline cudaError_t launch_pass_tma(const PassArgs& a, int sms, cudaStream_t st, 
   k<<<(int)g, kTmaThreads, L::kSmemBytes, st>>>(a);
   if (grid_out) *grid_out = (int)g;
   return cudaGetLastError();
+}
+
+// The persistent loop kernel needs every CTA resident at once: cooperative
+// launch (fails instead of deadlocking when the grid cannot be co-resident).
+template <typename XT, int C, int MODE>
+inline cudaError_t launch_loop_tma(const PassArgs& a, int sms, cudaStream_t st, int* grid_out,
+                                   int force_grid) {
+  using L = TmaLayout<XT, C, MODE == MODE_LUT>;
+  auto k = loop_tma_kernel<XT, C, MODE>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kSmemBytes);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kTmaThreads, L::kSmemBytes);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorCooperativeLaunchTooLarge;
+  long long g = (long long)per_sm * sms;
+  if (force_grid > 0 && force_grid < g) g = force_grid;
+  if (g > a.g.tiles_local) g = a.g.tiles_local;
+  if (g < 1) g = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)g);
+  cfg.blockDim = dim3(kTmaThreads);
+  cfg.dynamicSmemBytes = L::kSmemBytes;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, k, a);
+  if (grid_out) *grid_out = (int)g;
+  return e;
 }
 
 }  // namespace fcm

@@ -183,6 +183,16 @@ class FcmPlan:
         check(lib().fcm_download(self._h, ptr(u), ptr(lab)), self._h, "fcm_download")
         return u, lab
 
+    def profile(self) -> np.ndarray:
+        """Loop-kernel timeline of the last run (FCM_OPT_PROFILE): array [pass, cta, slot]
+        with slots 0 start, 1 claims done, 2 consumers done, 3 barrier released (ns), 4 tiles."""
+        cap = 64 * 8 * 1024 * 16
+        buf = np.zeros(cap, dtype=np.uint64)
+        passes, grid = ctypes.c_int32(), ctypes.c_int32()
+        check(lib().fcm_last_profile(self._h, ptr(buf), cap, ctypes.byref(passes), ctypes.byref(grid)),
+              self._h, "fcm_last_profile")
+        return buf[: passes.value * grid.value * 16].reshape(passes.value, grid.value, 16)
+
     def timing(self) -> dict:
         keys = ("loop_ms", "pass_ms", "prologue_ms", "passes_launched", "passes")
         buf = (ctypes.c_double * len(keys))()

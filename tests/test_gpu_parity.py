@@ -143,31 +143,69 @@ def test_iterate_matches_reference_contract():
     assert np.abs(u - r["u"]).max() <= U_ATOL
 
 
-@pytest.mark.parametrize("kernel,graph", [(0, 0), (1, 1), (1, 0), (2, 1)])
-def test_launch_modes_and_kernels_agree(kernel, graph):
-    """Device-side loop (CUDA graph + conditional node) vs host-driven batches,
-    and the TMA / register-staged / intensity-table pass kernels: same run."""
+@pytest.mark.parametrize("kernel,graph,loop,l2", [
+    (0, 1, 0, 1), (0, 0, 0, 1), (1, 1, 0, 1), (1, 0, 0, 1), (2, 1, 0, 1),
+    (2, 1, 1, 1), (3, 1, 1, 1), (0, 1, 1, 0), (0, 1, 1, 2), (0, 0, 0, 2)])
+def test_launch_modes_and_kernels_agree(kernel, graph, loop, l2):
+    """Persistent loop kernel (default) vs one launch per pass (CUDA graph with
+    a conditional node, or host-driven batches), the TMA / register-staged /
+    intensity-table / direct pass kernels, and the L2 policies: same run.
+    The loop kernel and the per-pass TMA kernel share the tree and the math,
+    so they agree bit for bit."""
     from paper_1601_00072_b200 import _lib
     r = run_case("phantom_c4")
     x = r["x"].astype(np.uint8)
 
-    def solve(kernel, graph):
+    def solve(kernel, graph, loop, l2):
         with pkg.FcmPlan(x.shape[0], 4, _lib.FCM_X_U8) as plan:
             plan.upload_pixels(x)
             plan.init_membership(r["seed"])
             plan.set_option(_lib.FCM_OPT_KERNEL, kernel)
             plan.set_option(_lib.FCM_OPT_GRAPH, graph)
+            plan.set_option(_lib.FCM_OPT_LOOP, loop)
+            plan.set_option(_lib.FCM_OPT_L2, l2)
             v, trace, k, conv = plan.run(2.0, r["epsilon"], r["max_iters"])
             u, lab = plan.download()
-        return v, trace, k, conv, u, lab
+            t = plan.timing()
+        return v, trace, k, conv, u, lab, t
 
-    base = solve(0, 1)
-    other = solve(kernel, graph)
+    base = solve(0, 1, 1, 1)
+    assert base[6]["passes_launched"] == 1  # one loop-kernel launch ran every pass
+    other = solve(kernel, graph, loop, l2)
     assert other[2] == base[2] == r["iterations"] and other[3] == base[3]
     assert np.allclose(other[0], base[0], rtol=1e-12)
     assert np.array_equal(other[5], base[5])
     if kernel == 0:
         assert other[0].tobytes() == base[0].tobytes() and other[1].tobytes() == base[1].tobytes()
+        assert other[4].tobytes() == base[4].tobytes()
+
+
+@pytest.mark.parametrize("c,m,float_pixels", [(3, 2.0, False), (8, 1.5, False), (5, 3.0, True), (16, 2.0, False)])
+def test_loop_kernel_matches_per_pass_bitwise(c, m, float_pixels):
+    """Loop kernel == per-pass launches for the m == 2 product form, the
+    intensity table (c=8, m=1.5), fp64 pixels and the generic c <= 16 path."""
+    from paper_1601_00072_b200 import _lib
+    x = mixture_pixels(200_003, c, seed=21 + c)
+    kind = _lib.FCM_X_F64 if float_pixels else _lib.FCM_X_U8
+    if float_pixels:
+        x = x + 0.25
+    else:
+        x = np.clip(np.rint(x), 0, 255).astype(np.uint8)
+
+    def solve(loop):
+        with pkg.FcmPlan(x.shape[0], c, kind) as plan:
+            plan.upload_pixels(x)
+            plan.init_membership(7)
+            plan.set_option(_lib.FCM_OPT_LOOP, loop)
+            out = plan.run(m, 1e-5, 300)
+            u, lab = plan.download()
+        return out, u, lab
+
+    (va, ta, ka, ca), ua, la = solve(1)
+    (vb, tb, kb, cb), ub, lb = solve(0)
+    assert ka == kb and ca == cb
+    assert va.tobytes() == vb.tobytes() and ta.tobytes() == tb.tobytes()
+    assert ua.tobytes() == ub.tobytes() and np.array_equal(la, lb)
 
 
 def test_graph_loop_reuse_and_max_iters():
@@ -229,3 +267,32 @@ def test_config2_volume_vs_oracle():
     assert np.abs(res.membership.u - ref["membership"]).max() <= U_ATOL
     assert np.array_equal(res.labels.labels, ref["labels"])
     assert np.allclose(np.array(res.objective_trace), ref["objective_trace"], rtol=TRACE_RTOL)
+
+
+def test_three_level_tree_loop_vs_per_pass_vs_shards_bitwise():
+    """A volume whose octants need a 3-level node tree (M > 1024 tiles): the
+    loop kernel (redundant upper levels after the grid barrier), one launch
+    per pass (CTA 0 climbs) and a 2-shard plan (NCCL-free peer finalize) give
+    the same bits."""
+    from paper_1601_00072_b200 import _lib
+    n = 25_000_003
+    geo = _lib.geometry(n)
+    assert geo["levels"] == 3
+    x = np.clip(np.rint(mixture_pixels(n, 3, seed=77)), 0, 255).astype(np.uint8)
+
+    def solve(loop, devices=None):
+        plan = pkg.FcmPlan(n, 3, _lib.FCM_X_U8, devices=devices) if devices else pkg.FcmPlan(n, 3, _lib.FCM_X_U8)
+        with plan:
+            plan.upload_pixels(x)
+            plan.init_membership(3)
+            plan.set_option(_lib.FCM_OPT_LOOP, loop)
+            out = plan.run(2.0, 1e-5, 100)
+            u, lab = plan.download()
+        return out, u, lab
+
+    (va, ta, ka, ca), ua, la = solve(1)
+    for other in (solve(0), solve(1, devices=[0, 0])):
+        (vb, tb, kb, cb), ub, lb = other
+        assert ka == kb and ca == cb
+        assert va.tobytes() == vb.tobytes() and ta.tobytes() == tb.tobytes()
+        assert ua.tobytes() == ub.tobytes() and np.array_equal(la, lb)

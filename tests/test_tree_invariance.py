@@ -27,7 +27,9 @@ def test_geometry_partitions_voxels(n):
     g1 = geometry(n, 1, 0)
     tile = g1["tile"]
     assert g1["n_local"] == n and g1["voxel0"] == 0
-    assert g1["T"] == -(-n // tile) and g1["T"] <= 8192 and g1["gpo"] <= 32
+    assert g1["T"] == -(-n // tile) and g1["T"] <= 8 * 32 ** 3
+    assert 1 <= g1["levels"] <= 3 and g1["M"] <= 32 ** g1["levels"]
+    assert g1["levels"] == 1 or g1["M"] > 32 ** (g1["levels"] - 1)
     assert tile >= 1024 and tile & (tile - 1) == 0
     for N in (2, 4, 8):
         covered = 0

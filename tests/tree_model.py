@@ -18,34 +18,40 @@ def warp_tree(vals, is_max):
     return x[0]
 
 
-def group_real_tiles(geo, o, g):
-    lo = o * geo["M"] + g * 32
-    hi = min(o * geo["M"] + min((g + 1) * 32, geo["M"]), geo["T"])
-    return max(0, hi - lo)
+def octant_real_nodes(geo, o, level):
+    rt = min(geo["M"], geo["T"] - o * geo["M"])
+    if rt <= 0:
+        return 0
+    span = 32 ** level
+    return -(-rt // span)
 
 
 def rank_root(tile_part, geo):
-    """tile_part: (T, nf) float64 partials of ALL global tiles; geo: one rank's geometry."""
-    T, M, gpo = geo["T"], geo["M"], geo["gpo"]
+    """tile_part: (T, nf) float64 partials of ALL global tiles; geo: one rank's geometry.
+
+    Per octant a 32-ary tree of geo["levels"] levels over its M tiles (node j of
+    level l reduces children 32j..32j+31 of level l-1 with warp_tree; unreal
+    children contribute 0.0), then a warp tree over the rank's octant roots.
+    """
+    T, M, L = geo["T"], geo["M"], geo["levels"]
     nf = tile_part.shape[1]
     oct_roots = []
     for o in range(geo["oct0"], geo["oct0"] + geo["noct"]):
-        groups = []
-        for g in range(gpo):
-            fields = []
-            for f in range(nf):
-                leaves = []
-                for lane in range(32):
-                    leaf = g * 32 + lane
-                    real = leaf < M and o * M + leaf < T
-                    leaves.append(float(tile_part[o * M + leaf, f]) if real else 0.0)
-                fields.append(warp_tree(leaves, f == nf - 1))
-            groups.append(fields)
-        fields = []
-        for f in range(nf):
-            leaves = [groups[g][f] if (g < gpo and group_real_tiles(geo, o, g) > 0) else 0.0 for g in range(32)]
-            fields.append(warp_tree(leaves, f == nf - 1))
-        oct_roots.append(fields if o * M < T else [0.0] * nf)
+        if o * M >= T:
+            oct_roots.append([0.0] * nf)
+            continue
+        level = [tile_part[o * M + t] for t in range(octant_real_nodes(geo, o, 0))]
+        for lv in range(1, L + 1):
+            n_nodes = -(-M // 32 ** lv)
+            nxt = []
+            for j in range(n_nodes):
+                if j >= octant_real_nodes(geo, o, lv):
+                    break
+                kids = [level[k] if k < len(level) else None for k in range(32 * j, 32 * j + 32)]
+                nxt.append([warp_tree([kd[f] if kd is not None else 0.0 for kd in kids], f == nf - 1)
+                            for f in range(nf)])
+            level = nxt
+        oct_roots.append(level[0])
     return np.array([warp_tree([r[f] for r in oct_roots], f == nf - 1) for f in range(nf)])
 
 
