@@ -76,7 +76,7 @@ class ClockSampler:
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+              "clocks_event_reasons.sw_power_cap,power.draw")
 
     def __init__(self, device: int):
         self.device = device
@@ -112,7 +112,7 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        sm, smax, reasons = [], [], set()
+        sm, smax, reasons, pw = [], [], set(), []
         names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
         for ln in self.lines:
             parts = [p.strip() for p in ln.split(",")]
@@ -126,10 +126,14 @@ class ClockSampler:
             for nm, val in zip(names, parts[2:6]):
                 if val.lower().startswith("active"):
                     reasons.add(nm)
+            try:
+                pw.append(float(parts[6]))
+            except (ValueError, IndexError):
+                pass
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(smax), "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "power_w": statistics.median(pw) if pw else None}
 
 
 def make_volume(shape, rank_slice=None):
@@ -337,7 +341,8 @@ def run_ours(args, rank, world, local_rank, dist):
             "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured" else peak_kind,
             "bytes_per_voxel_iter": B,
             "kernel": ("loop_tma_kernel" if looped else ("pass_kernel" if args.kernel == "ldg" else "pass_tma_kernel"))
-            + "<uint8_t,%d,%s>" % (c, "MODE_M2" if m == 2.0 and args.kernel in ("tma", "direct", "ldg")
+            + "<uint8_t,%d,%s>" % (c, ("MODE_LUT2" if args.kernel == "tma" else "MODE_M2")
+                                   if m == 2.0 and args.kernel in ("tma", "direct", "ldg")
                                    else ("MODE_LUT" if args.kernel in ("tma", "lut") else "MODE_GEN")),
             "timing": ("CUDA events around the persistent loop kernel (one launch = every pass of a solve, grid "
                        "barriers included) on its launching stream, timed region" if looped else

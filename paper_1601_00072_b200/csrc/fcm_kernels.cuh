@@ -497,6 +497,8 @@ cudaError_t launch_pass_c(int xkind, int mode, const PassArgs& a, int sms, cudaS
       // -> per-pass intensity table (C <= 8); variant 3 -> direct math always.
       if (C <= 8 && variant != 3 && (variant == 2 || !m2))
         return launch_pass_tma<uint8_t, C, (C <= 8 ? MODE_LUT : MODE_GEN)>(a, sms, st, grid_out, force_grid);
+      if (C <= 8 && m2 && variant == 0)
+        return launch_pass_tma<uint8_t, C, (C <= 8 ? MODE_LUT2 : MODE_GEN)>(a, sms, st, grid_out, force_grid);
       return m2 ? launch_pass_tma<uint8_t, C, MD>(a, sms, st, grid_out, force_grid)
                 : launch_pass_tma<uint8_t, C, MODE_GEN>(a, sms, st, grid_out, force_grid);
     }
@@ -528,6 +530,8 @@ cudaError_t launch_loop_c(int xkind, int mode, const PassArgs& a, int sms, cudaS
   if (xkind == XK_U8) {
     if (C <= 8 && variant != 3 && (variant == 2 || !m2))
       return launch_loop_tma<uint8_t, C, (C <= 8 ? MODE_LUT : MODE_GEN)>(a, sms, st, grid_out, force_grid);
+    if (C <= 8 && m2 && variant == 0)
+      return launch_loop_tma<uint8_t, C, (C <= 8 ? MODE_LUT2 : MODE_GEN)>(a, sms, st, grid_out, force_grid);
     return m2 ? launch_loop_tma<uint8_t, C, MD>(a, sms, st, grid_out, force_grid)
               : launch_loop_tma<uint8_t, C, MODE_GEN>(a, sms, st, grid_out, force_grid);
   }

@@ -56,6 +56,19 @@ __device__ __forceinline__ void mbar_arrive_tx(uint32_t bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
+// try_wait with a suspend-time hint: the thread sleeps in hardware until the
+// phase completes or about `ns` nanoseconds pass (no busy polling).
+__device__ __forceinline__ bool mbar_wait_for(uint32_t bar, uint32_t parity, uint32_t ns) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity), "r"(ns)
+      : "memory");
+  return ok != 0;
+}
 __device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
@@ -105,8 +118,7 @@ __device__ __forceinline__ double u8_to_f64(uint32_t byte) {
 // equal-share rule applies, _kernels.pyx:103-113).  The objective term
 // sum_j u_j^2 D_j collapses to prod_k D_k / sum_k P_k.
 template <int C>
-__device__ __forceinline__ void voxel_m2_u8(double xd, const double* v, float uo_f[C], float* un,
-                                            double* acc, uint32_t& dmax_hi, bool valid) {
+__device__ __forceinline__ void m2_membership(double xd, const double* v, double* u, double& obj) {
   double D[C];
 #pragma unroll
   for (int j = 0; j < C; ++j) {
@@ -127,7 +139,6 @@ __device__ __forceinline__ void voxel_m2_u8(double xd, const double* v, float uo
   }
   P[0] = suf;
   const double all = pre[C - 1];
-  double u[C];
   if (all != 0.0) {
     double Q = P[0];
 #pragma unroll
@@ -135,7 +146,7 @@ __device__ __forceinline__ void voxel_m2_u8(double xd, const double* v, float uo
     const double R = rcp64(Q);
 #pragma unroll
     for (int j = 0; j < C; ++j) u[j] = P[j] * R;
-    if (valid) acc[2 * C] += all * R;
+    obj = all * R;
   } else {
     int zc = 0;
 #pragma unroll
@@ -143,7 +154,15 @@ __device__ __forceinline__ void voxel_m2_u8(double xd, const double* v, float uo
     const double share = 1.0 / (double)zc;
 #pragma unroll
     for (int j = 0; j < C; ++j) u[j] = D[j] == 0.0 ? share : 0.0;
+    obj = 0.0;  // sum_j u_j^2 D_j with every weight on a zero distance
   }
+}
+
+// Eq. 3 / delta / store terms of one voxel from its fp64 memberships.
+template <int C>
+__device__ __forceinline__ void m2_fold(double xd, const double* u, double obj, const float* uo_f, float* un,
+                                        double* acc, uint32_t& dmax_hi, bool valid) {
+  if (valid) acc[2 * C] += obj;
 #pragma unroll
   for (int j = 0; j < C; ++j) {
     const double w = u[j] * u[j];
@@ -155,6 +174,14 @@ __device__ __forceinline__ void voxel_m2_u8(double xd, const double* v, float uo
     }
     un[j] = (float)u[j];
   }
+}
+
+template <int C>
+__device__ __forceinline__ void voxel_m2_u8(double xd, const double* v, float uo_f[C], float* un,
+                                            double* acc, uint32_t& dmax_hi, bool valid) {
+  double u[C], obj;
+  m2_membership<C>(xd, v, u, obj);
+  m2_fold<C>(xd, u, obj, uo_f, un, acc, dmax_hi, valid);
 }
 
 // General path: robust normalised form (membership()) and the reference's
@@ -200,12 +227,24 @@ struct LutLayout {
   static constexpr int kBytes = kJOff + 256 * 8;
 };
 
-template <typename XT, int C, bool LUT = false>
+// m == 2 table (MODE_LUT2): per intensity the fp64 product-form memberships
+// u_0..u_{C-1} and the objective term, as double2 chunks interleaved like
+// LutLayout (chunk k of intensity b at (k*256 + b)*16).  Entries are exactly
+// what m2_membership returns, so the table path is bit-identical to the
+// per-voxel product form while the stream does no division per voxel.
+template <int C>
+struct Lut2Layout {
+  static constexpr int K2 = (C + 2) / 2;  // C memberships + objective term
+  static constexpr int kBytes = K2 * 256 * 16;
+};
+
+template <typename XT, int C, int MODE = MODE_M2>
 struct TmaLayout {
   static constexpr int kXBytes = kChunk * (int)sizeof(XT);
   static constexpr int kUBytes = kChunk * 4;
   static constexpr int kStageBytes = kXBytes + C * kUBytes;
-  static constexpr int kLutBytes = LUT ? LutLayout<C>::kBytes : 0;
+  static constexpr int kLutBytes =
+      MODE == MODE_LUT ? LutLayout<C>::kBytes : (MODE == MODE_LUT2 ? Lut2Layout<C>::kBytes : 0);
   static constexpr int kStages0 = (kStageBudget - kLutBytes) / kStageBytes;
   static constexpr int kStages = kStages0 < 2 ? 2 : (kStages0 > 8 ? 8 : kStages0);
   static constexpr int kRingBytes = kStages * kStageBytes;
@@ -287,10 +326,10 @@ __device__ __forceinline__ void probe(const PassArgs& a, unsigned it, int k, uin
 // One elected thread: claim tiles from `counter` until the rank's tiles are
 // exhausted, stream every chunk of x and of the c planes of u_{k-1} into the
 // ring, then post the end-of-pass marker.
-template <typename XT, int C, bool LUT>
+template <typename XT, int C, int MODE>
 __device__ __forceinline__ int tma_produce(const PassArgs& a, uint8_t* smem, Pipe& ps, unsigned* counter,
                                            unsigned it = 0) {
-  using L = TmaLayout<XT, C, LUT>;
+  using L = TmaLayout<XT, C, MODE>;
   constexpr int S = L::kStages;
   const uint32_t bar0 = smem_u32(smem + L::kBarOff);
   StageMeta* meta = reinterpret_cast<StageMeta*>(smem + L::kMetaOff);
@@ -381,6 +420,24 @@ __device__ __forceinline__ void tma_build_lut(uint8_t* lut, const double* v, int
   red_sync<true>();
 }
 
+// m == 2 table: entry b = tid is m2_membership at x = b (the per-voxel
+// product form, bit for bit).  Ends with a consumer barrier.
+template <int C>
+__device__ __forceinline__ void tma_build_lut2(uint8_t* lut, const double* v) {
+  constexpr int K2 = Lut2Layout<C>::K2;
+  const int tid = threadIdx.x;
+  double e[2 * K2];
+#pragma unroll
+  for (int j = 0; j < 2 * K2; ++j) e[j] = 0.0;
+  double obj;
+  m2_membership<C>((double)tid, v, e, obj);
+  e[C] = obj;
+#pragma unroll
+  for (int k = 0; k < K2; ++k)
+    reinterpret_cast<double2*>(lut)[k * 256 + tid] = make_double2(e[2 * k], e[2 * k + 1]);
+  red_sync<true>();
+}
+
 // ------------------------------------------------------------ consumers ---
 // The 8 consumer warps: per stage, copy 4 voxels per thread to registers,
 // release the stage, evaluate Eq. 4, store u_k (in place over u_{k-1}: each
@@ -392,7 +449,8 @@ __device__ __forceinline__ void tma_consume(const PassArgs& a, uint8_t* smem, Pi
                                             RedSlots<2 * C + 2>& rs, Pipe& sp, const double* v,
                                             const Powers& pw) {
   constexpr bool LUT = MODE == MODE_LUT;
-  using L = TmaLayout<XT, C, LUT>;
+  constexpr bool LUT2 = MODE == MODE_LUT2;
+  using L = TmaLayout<XT, C, MODE>;
   using LL = LutLayout<C>;
   constexpr int S = L::kStages;
   const int tid = threadIdx.x;
@@ -482,6 +540,17 @@ __device__ __forceinline__ void tma_consume(const PassArgs& a, uint8_t* smem, Pi
           }
           nq[j] = ufv[j];
         }
+      } else if (LUT2) {
+        const int b = (int)(xd[q] - 0.0);
+        constexpr int K2 = Lut2Layout<C>::K2;
+        double e[2 * K2];
+#pragma unroll
+        for (int k = 0; k < K2; ++k) {
+          const double2 w2 = reinterpret_cast<const double2*>(lut)[k * 256 + b];
+          e[2 * k] = w2.x;
+          e[2 * k + 1] = w2.y;
+        }
+        m2_fold<C>(xd[q], e, e[C], uq, nq, acc, dmax_hi, valid);
       } else if (MODE == MODE_M2 && sizeof(XT) == 1 && C <= 8)
         voxel_m2_u8<C>(xd[q], v, uq, nq, acc, dmax_hi, valid);
       else
@@ -612,8 +681,12 @@ __device__ __forceinline__ void tma_reduce(const PassArgs& a, RedSlots<2 * C + 2
   int zb = 0;
   bool slots_done = false;
   uint64_t n_poll = 0, n_node = 0;
+  uint32_t backoff = 64;
   while (!slots_done || za < NA || zb < NB) {
-    if (!slots_done && mbar_test(smem_u32(&rs.full[sp.stage]), sp.phase)) {
+    // next slot: sleep in hardware until it fills (bounded while a node is
+    // pending, so the node is still polled about every microsecond)
+    if (!slots_done && ((za < NA || zb < NB) ? mbar_wait_for(smem_u32(&rs.full[sp.stage]), sp.phase, 1000)
+                                             : (mbar_wait(smem_u32(&rs.full[sp.stage]), sp.phase), true))) {
       const int t = rs.tile[sp.stage];
       if (t >= 0) {
         for (int f = lane; f < nf; f += 32) {  // nf <= 34
@@ -641,7 +714,6 @@ __device__ __forceinline__ void tma_reduce(const PassArgs& a, RedSlots<2 * C + 2
     } else if (zb < NB) {
       upper_node(g, zb, l, lo, j);
     } else {
-      __nanosleep(64);
       continue;
     }
     const int oct = g.oct0 + lo;
@@ -666,8 +738,10 @@ __device__ __forceinline__ void tma_reduce(const PassArgs& a, RedSlots<2 * C + 2
     if (advance) {
       if (za < NA) za += strideA;
       else ++zb;
-    } else {
-      __nanosleep(64);
+      backoff = 64;
+    } else if (slots_done) {
+      __nanosleep(backoff);  // pass drained: poll the pending node with a short backoff
+      backoff = min(backoff * 2, 512u);
     }
   }
   if (!LOOP && cta0) {
@@ -690,86 +764,73 @@ __device__ __forceinline__ void tma_reduce(const PassArgs& a, RedSlots<2 * C + 2
 
 // The adjacent-pair tree over 32 children (identical association to
 // warp_tree: ((c0+c1)+(c2+c3))+... up to (c0..15)+(c16..31)), evaluated by ONE
-// lane from memory (child i at p[i*stride]; children >= nreal count as 0.0):
-// no shuffles, so a warp evaluates up to 32 fields side by side.
-template <bool GLOBAL>
-__device__ __forceinline__ double tree8(const double* p, int64_t stride, int i0, int nreal, bool mx) {
-  double v[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i)
-    v[i] = (i0 + i < nreal) ? (GLOBAL ? __ldcg(p + (int64_t)(i0 + i) * stride) : p[(int64_t)(i0 + i) * stride]) : 0.0;
-  return combine(combine(combine(v[0], v[1], mx), combine(v[2], v[3], mx), mx),
-                 combine(combine(v[4], v[5], mx), combine(v[6], v[7], mx), mx), mx);
-}
+// thread from memory (child i at p[i*stride]; children >= nreal count as
+// 0.0): no shuffles, all loads in flight at once.
 template <bool GLOBAL>
 __device__ __forceinline__ double tree32(const double* p, int64_t stride, int nreal, bool mx) {
-  const double t0 = tree8<GLOBAL>(p, stride, 0, nreal, mx);
-  const double t1 = nreal > 8 ? tree8<GLOBAL>(p, stride, 8, nreal, mx) : 0.0;
-  const double t2 = nreal > 16 ? tree8<GLOBAL>(p, stride, 16, nreal, mx) : 0.0;
-  const double t3 = nreal > 24 ? tree8<GLOBAL>(p, stride, 24, nreal, mx) : 0.0;
-  return combine(combine(t0, t1, mx), combine(t2, t3, mx), mx);
+  double v[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i)
+    v[i] = i < nreal ? (GLOBAL ? __ldcg(p + (int64_t)i * stride) : p[(int64_t)i * stride]) : 0.0;
+#pragma unroll
+  for (int s2 = 1; s2 < 32; s2 <<= 1)
+#pragma unroll
+    for (int i = 0; i < 32; i += 2 * s2) v[i] = combine(v[i], v[i + s2], mx);
+  return v[0];
 }
 
 // Loop kernel, after the grid barrier of pass `it`: every CTA reduces the
 // levels above 1 from the published level-1 results (l1, [noct][nodes[1]][nf]),
 // the same fixed tree as everywhere else, into root[] -- redundantly, so no
-// further cross-CTA hop is needed.  Lane = field (tree32), warps share the
-// nodes of a level.  All kTmaThreads threads call it; scratch is the (idle)
-// stage ring.
+// further cross-CTA hop is needed.  Each (node, field) pair is one thread's
+// tree32; all kTmaThreads threads call it; scratch is the (idle) stage ring.
 template <int NF>
 __device__ __forceinline__ void loop_upper(const PassArgs& a, const double* l1, double* scratch,
                                            double (*oroot)[NF], double* root) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  constexpr int kW = kTmaThreads / 32;
+  const int tid = threadIdx.x;
   const int nf = 2 * a.c + 2;
   const Geometry& g = a.g;
   const int per = g.levels == 3 ? g.nodes[2] : 1;
   // step 1: level-2 nodes (L == 3) or octant roots (L == 2) from level-1 results
   if (g.levels >= 2) {
-    for (int item = warp; item < g.noct * per; item += kW) {
+    for (int pr = tid; pr < g.noct * per * nf; pr += kTmaThreads) {
+      const int item = pr / nf, f = pr - item * nf;
       const int lo = item / per, k = item - lo * per;
       const int oct = g.oct0 + lo;
       const int nreal = (int64_t)oct * g.M < g.T ? node_real_children(g, oct, 2, k) : 0;
-      const double* src = l1 + ((int64_t)lo * g.nodes[1] + (int64_t)k * kFan) * nf;
-      for (int f = lane; f < nf; f += 32)
-        scratch[(int64_t)item * NF + f] = nreal ? tree32<true>(src + f, nf, nreal, f == nf - 1) : 0.0;
+      const double* src = l1 + ((int64_t)lo * g.nodes[1] + (int64_t)k * kFan) * nf + f;
+      scratch[(int64_t)item * NF + f] = nreal ? tree32<true>(src, nf, nreal, f == nf - 1) : 0.0;
     }
+    __syncthreads();
   }
-  __syncthreads();
   // step 2: octant roots
-  for (int lo = warp; lo < g.noct; lo += kW) {
+  for (int pr = tid; pr < g.noct * nf; pr += kTmaThreads) {
+    const int lo = pr / nf, f = pr - lo * nf;
     const int oct = g.oct0 + lo;
-    const bool oreal = (int64_t)oct * g.M < g.T;
-    for (int f = lane; f < nf; f += 32) {
-      double r = 0.0;
-      if (oreal) {
-        if (g.levels == 1) r = __ldcg(l1 + (int64_t)lo * nf + f);  // the level-1 node is the octant root
-        else if (g.levels == 2) r = scratch[(int64_t)lo * NF + f];
-        else r = tree32<false>(scratch + (int64_t)lo * per * NF + f, NF, (int)octant_real_nodes(g, oct, 2), f == nf - 1);
-      }
-      oroot[lo][f] = r;
+    double r = 0.0;
+    if ((int64_t)oct * g.M < g.T) {
+      if (g.levels == 1) r = __ldcg(l1 + (int64_t)lo * nf + f);  // the level-1 node is the octant root
+      else if (g.levels == 2) r = scratch[(int64_t)lo * NF + f];
+      else r = tree32<false>(scratch + (int64_t)lo * per * NF + f, NF, (int)octant_real_nodes(g, oct, 2), f == nf - 1);
     }
+    oroot[lo][f] = r;
   }
   __syncthreads();
-  // step 3: the rank root over the rank's octants
-  if (warp == 0) {
-    int nreal = 0;
-    for (int lo = 0; lo < g.noct; ++lo) nreal += ((int64_t)(g.oct0 + lo) * g.M < g.T) ? 1 : 0;
-    for (int f = lane; f < nf; f += 32) {
-      double v[8];
+  // step 3: the rank root over the rank's octants (a pair tree over 8 leaves)
+  for (int f = tid; f < nf; f += kTmaThreads) {
+    double v[8];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) v[i] = i < nreal ? oroot[i][f] : 0.0;
-      const bool mx = f == nf - 1;
-      root[f] = combine(combine(combine(v[0], v[1], mx), combine(v[2], v[3], mx), mx),
-                        combine(combine(v[4], v[5], mx), combine(v[6], v[7], mx), mx), mx);
-    }
+    for (int i = 0; i < 8; ++i) v[i] = (i < g.noct && (int64_t)(g.oct0 + i) * g.M < g.T) ? oroot[i][f] : 0.0;
+    const bool mx = f == nf - 1;
+    root[f] = combine(combine(combine(v[0], v[1], mx), combine(v[2], v[3], mx), mx),
+                      combine(combine(v[4], v[5], mx), combine(v[6], v[7], mx), mx), mx);
   }
   __syncthreads();
 }
 
-template <typename XT, int C, bool LUT>
+template <typename XT, int C, int MODE>
 __device__ __forceinline__ void tma_init_barriers(uint8_t* smem, RedSlots<2 * C + 2>& rs) {
-  using L = TmaLayout<XT, C, LUT>;
+  using L = TmaLayout<XT, C, MODE>;
   const uint32_t bar0 = smem_u32(smem + L::kBarOff);
   for (int s = 0; s < L::kStages; ++s) {
     mbar_init(bar0 + 8u * s, 1);
@@ -792,7 +853,7 @@ __device__ __forceinline__ void load_centers(const Control* ctl, int c, double* 
 template <typename XT, int C, int MODE>
 __global__ void __launch_bounds__(kTmaThreads, 2) pass_tma_kernel(PassArgs a) {
   constexpr bool LUT = MODE == MODE_LUT;
-  using L = TmaLayout<XT, C, LUT>;
+  using L = TmaLayout<XT, C, MODE>;
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ RedSlots<2 * C + 2> rs;
   __shared__ int s_done;
@@ -810,7 +871,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) pass_tma_kernel(PassArgs a) {
     }
     s_done = done;
     if (!done) {
-      tma_init_barriers<XT, C, LUT>(smem, rs);
+      tma_init_barriers<XT, C, MODE>(smem, rs);
       if (blockIdx.x == 0) a.ctl->tile_next[(a.seq + 1) & 1] = 0u;
     }
   }
@@ -818,7 +879,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) pass_tma_kernel(PassArgs a) {
   if (s_done) return;
   Pipe ps, sp;
   if (tid >= kThreads) {
-    if (tid == kProducerTid) tma_produce<XT, C, LUT>(a, smem, ps, &a.ctl->tile_next[a.seq & 1]);
+    if (tid == kProducerTid) tma_produce<XT, C, MODE>(a, smem, ps, &a.ctl->tile_next[a.seq & 1]);
     else if ((tid >> 5) == kReducerWarp)
       tma_reduce<C, false>(a, rs, sp, &a.ctl->tile_next[a.seq & 1], nullptr);
     return;
@@ -828,6 +889,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) pass_tma_kernel(PassArgs a) {
   load_centers<C>(a.ctl, c, v);
   const Powers pw = load_powers(a);
   if (LUT) tma_build_lut<C>(smem + L::kLutOff, v, c, pw);
+  if (MODE == MODE_LUT2) tma_build_lut2<C>(smem + L::kLutOff, v);
   tma_consume<XT, C, MODE>(a, smem, ps, rs, sp, v, pw);
 }
 
@@ -858,6 +920,7 @@ __device__ __forceinline__ bool grid_barrier(Control* ctl, unsigned it, unsigned
   }
   const uint64_t t0 = global_ns();
   while (ld_acquire_u32(&ctl->epoch) < it) {
+    __nanosleep(32);
     if (global_ns() - t0 > 4000000000ull) {
       ctl->dead = -3;
       ctl->done = 1;
@@ -918,7 +981,7 @@ template <typename XT, int C, int MODE>
 __global__ void __launch_bounds__(kTmaThreads, 2) loop_tma_kernel(PassArgs a) {
   constexpr bool LUT = MODE == MODE_LUT;
   constexpr int NF = 2 * C + 2;
-  using L = TmaLayout<XT, C, LUT>;
+  using L = TmaLayout<XT, C, MODE>;
   static_assert(L::kRingBytes >= kOctants * kFan * NF * 8, "ring too small for the upper-level scratch");
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ RedSlots<NF> rs;
@@ -928,7 +991,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) loop_tma_kernel(PassArgs a) {
   const int tid = threadIdx.x;
   const int c = C <= 8 ? C : a.c;
   if (tid == 0) {
-    tma_init_barriers<XT, C, LUT>(smem, rs);
+    tma_init_barriers<XT, C, MODE>(smem, rs);
     s_done = *(volatile int*)&a.ctl->done;
     for (int j = 0; j < c; ++j) vsh[j] = __ldcg(&a.ctl->v[j]);
   }
@@ -942,7 +1005,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) loop_tma_kernel(PassArgs a) {
     if (tid >= kThreads) {
       if (tid == kProducerTid) {
         fence_proxy_async_global();
-        const int n = tma_produce<XT, C, LUT>(a, smem, ps, &a.ctl->tile_next[1], it);  // zeroed by the prologue
+        const int n = tma_produce<XT, C, MODE>(a, smem, ps, &a.ctl->tile_next[1], it);  // zeroed by the prologue
         probe(a, it, 1, global_ns());
         probe(a, it, 4, (uint64_t)n);
         unsigned smid;
@@ -957,6 +1020,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) loop_tma_kernel(PassArgs a) {
 #pragma unroll
       for (int j = 0; j < C; ++j) v[j] = j < c ? vsh[j] : 0.0;
       if (LUT) tma_build_lut<C>(smem + L::kLutOff, v, c, pw);
+      if (MODE == MODE_LUT2) tma_build_lut2<C>(smem + L::kLutOff, v);
       tma_consume<XT, C, MODE>(a, smem, ps, rs, sp, v, pw);
       if (tid == 0) probe(a, it, 2, global_ns());
     }
@@ -979,7 +1043,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) loop_tma_kernel(PassArgs a) {
 template <typename XT, int C, int MODE>
 inline cudaError_t launch_pass_tma(const PassArgs& a, int sms, cudaStream_t st, int* grid_out,
                                    int force_grid) {
-  using L = TmaLayout<XT, C, MODE == MODE_LUT>;
+  using L = TmaLayout<XT, C, MODE>;
   auto k = pass_tma_kernel<XT, C, MODE>;
   int dev = 0;
   cudaGetDevice(&dev);
@@ -1005,7 +1069,7 @@ inline cudaError_t launch_pass_tma(const PassArgs& a, int sms, cudaStream_t st, 
 template <typename XT, int C, int MODE>
 inline cudaError_t launch_loop_tma(const PassArgs& a, int sms, cudaStream_t st, int* grid_out,
                                    int force_grid) {
-  using L = TmaLayout<XT, C, MODE == MODE_LUT>;
+  using L = TmaLayout<XT, C, MODE>;
   auto k = loop_tma_kernel<XT, C, MODE>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kSmemBytes);
   if (e != cudaSuccess) return e;

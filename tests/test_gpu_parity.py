@@ -175,7 +175,7 @@ def test_launch_modes_and_kernels_agree(kernel, graph, loop, l2):
     assert other[2] == base[2] == r["iterations"] and other[3] == base[3]
     assert np.allclose(other[0], base[0], rtol=1e-12)
     assert np.array_equal(other[5], base[5])
-    if kernel == 0:
+    if kernel in (0, 3):  # the m == 2 table path is the per-voxel product form, bit for bit
         assert other[0].tobytes() == base[0].tobytes() and other[1].tobytes() == base[1].tobytes()
         assert other[4].tobytes() == base[4].tobytes()
 

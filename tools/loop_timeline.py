@@ -17,6 +17,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="C2")
 ap.add_argument("--l2", type=int, default=1)
 ap.add_argument("--kernel", type=int, default=0)
+ap.add_argument("--warm", type=int, default=3, help="solves before the profiled one (steady state: ~40)")
 args = ap.parse_args()
 shape, c, m, eps = bench.CONFIGS[args.config]
 x = bench.make_volume(shape)
@@ -25,7 +26,7 @@ plan.upload_pixels(x)
 plan.init_membership(0)
 plan.set_option(_lib.FCM_OPT_L2, args.l2)
 plan.set_option(_lib.FCM_OPT_KERNEL, args.kernel)
-for _ in range(3):
+for _ in range(args.warm):
     plan.run(m, eps, 500)
 plan.set_option(_lib.FCM_OPT_PROFILE, 1)
 v, trace, k, conv = plan.run(m, eps, 500)
