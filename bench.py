@@ -60,9 +60,10 @@ def load_peaks():
         return 6650.0, "fallback"
 
 
-def load_traffic(config: str):
-    """Per-launch dram bytes of the pass kernel from the committed ncu summary, if any."""
-    p = os.path.join(REPO, "profiles", f"ncu_pass_{config}.json")
+def load_traffic(config: str, kernel: str = "pass"):
+    """Per-launch dram bytes of the dominant kernel from the committed ncu summary, if any
+    (profiles/ncu_loop_<config>.json: one loop-kernel launch = every pass of a solve)."""
+    p = os.path.join(REPO, "profiles", f"ncu_{kernel}_{config}.json")
     try:
         with open(p) as f:
             d = json.load(f)
@@ -303,7 +304,7 @@ def run_ours(args, rank, world, local_rank, dist):
         achieved = B * n_pass * iters[0] / (loop_kernel_ms / 1e3) / 1e9 if loop_kernel_ms > 0 else None
     else:
         achieved = B * n_pass / (pass_avg / 1e3) / 1e9 if pass_avg > 0 else None
-    traffic = load_traffic(args.config)
+    traffic = load_traffic(args.config, "loop" if looped else "pass")
     out = {
         "metric": "voxel-iterations/sec",
         "value": value,
