@@ -210,6 +210,7 @@ def run_ours(args, rank, world, local_rank, dist):
     plan.init_membership(0)
     plan.set_option(_lib.FCM_OPT_KERNEL, KERNELS[args.kernel])
     plan.set_option(_lib.FCM_OPT_LOOP, 0 if args.no_loop else 1)
+    plan.set_option(_lib.FCM_OPT_SEED_PASS, 0 if args.no_seed_pass else 1)
 
     def barrier():
         if world > 1:
@@ -237,14 +238,15 @@ def run_ours(args, rank, world, local_rank, dist):
             t = plan.timing()
             loop_ms.append(t["loop_ms"])
             iters.append(k)
-            launched.append(int(t["passes_launched"]) + 1)
+            launched.append(int(t["passes_launched"]) + (0 if t.get("seeded_in_loop") else 1))
             kern_ms.append(t["pass_ms"] * k)  # loop kernel: CUDA events around its launch
         t_wall = time.perf_counter() - t_wall
     barrier()
     total_ms = max_over_ranks(sum(loop_ms))
     info = plan.info()
 
-    looped = launched[0] == 2  # prologue + one persistent loop-kernel launch
+    seeded = bool(t.get("seeded_in_loop", 0))
+    looped = int(t["passes_launched"]) == 1  # one persistent loop-kernel launch ran every pass
     loop_kernel_ms = max_over_ranks(float(np.mean(kern_ms)))
 
     # ---- per-pass kernel timing (A/B): the same solves launched pass by pass
@@ -301,7 +303,9 @@ def run_ours(args, rank, world, local_rank, dist):
     if looped:
         # dominant kernel = loop_tma_kernel: one launch runs every pass of a
         # solve; algorithmic bytes per launch = B * n_local * iterations
-        achieved = B * n_pass * iters[0] / (loop_kernel_ms / 1e3) / 1e9 if loop_kernel_ms > 0 else None
+        # (+ the seeded start when the loop kernel ran it as pass 0: x read + u_0 written)
+        seed_bytes = (1 + 4 * c) * n_pass if seeded else 0
+        achieved = (B * n_pass * iters[0] + seed_bytes) / (loop_kernel_ms / 1e3) / 1e9 if loop_kernel_ms > 0 else None
     else:
         achieved = B * n_pass / (pass_avg / 1e3) / 1e9 if pass_avg > 0 else None
     traffic = load_traffic(args.config, "loop" if looped else "pass")
@@ -410,6 +414,8 @@ def main():
     ap.add_argument("--config", default="C4", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-seed-pass", action="store_true",
+                    help="separate prologue kernel for the seeded start instead of the loop kernel's pass 0")
     ap.add_argument("--no-loop", action="store_true",
                     help="one launch per pass (CUDA graph with a conditional node) instead of the persistent loop kernel")
     ap.add_argument("--kernel", default="tma", choices=sorted(KERNELS),

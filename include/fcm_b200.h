@@ -65,7 +65,9 @@ typedef enum {
                           between passes; 0: one launch per pass (graph or host-driven) */
   FCM_OPT_L2 = 7,      /* 0: stream x/u with evict-first stores; 1 (default): keep them in L2
                           (evict_last policy) when they fit; 2: always */
-  FCM_OPT_PROFILE = 8  /* 1: the loop kernel records a per-CTA timeline (fcm_last_profile) */
+  FCM_OPT_PROFILE = 8, /* 1: the loop kernel records a per-CTA timeline (fcm_last_profile) */
+  FCM_OPT_SEED_PASS = 9 /* 1 (default): with a seeded start the loop kernel generates u_0 as its
+                           pass 0; 0: a separate prologue kernel does */
 } fcm_option;
 
 typedef struct fcm_plan fcm_plan;
@@ -138,9 +140,12 @@ int fcm_run(fcm_plan* plan, double m, double epsilon, int32_t max_iters, double*
  * of the plan's voxel range.  Either pointer may be NULL. */
 int fcm_download(fcm_plan* plan, double* u_aos_out, int32_t* labels_out);
 
-/* out[0..]: ms of the last fcm_run's device loop (prologue + passes, CUDA
- * events), mean ms per pass (when FCM_OPT_TIMING), prologue ms, passes
- * launched, passes that did work. */
+/* out[0..]: ms of the last fcm_run's device loop (start + passes, CUDA
+ * events), ms per pass (FCM_OPT_TIMING: mean pass-kernel time; loop kernel:
+ * its duration / passes, the seeded start included), prologue-kernel ms
+ * (0 when the loop kernel generated u_0 itself), kernel launches of the
+ * loop (1 for the loop kernel), passes that did work, 1 if the loop kernel
+ * ran the seeded start as its pass 0. */
 int fcm_last_timing(const fcm_plan* plan, double* out, int32_t count);
 
 /* Loop-kernel timeline of the last fcm_run with FCM_OPT_PROFILE (diagnostics):

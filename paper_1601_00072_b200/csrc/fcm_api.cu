@@ -113,6 +113,7 @@ struct fcm_plan {
   int use_loop = 1;
   int l2_mode = 1;  // 0 never keep x/u in L2, 1 when they fit (default), 2 always
   int profile = 0;  // record the loop kernel's per-CTA timeline
+  int seed_pass = 1;  // loop kernel generates the seeded u_0 as its pass 0
   uint64_t* prof = nullptr;
   int prof_passes = 0, prof_grid = 0;
   bool capturing = false;
@@ -130,6 +131,7 @@ struct fcm_plan {
   cudaEvent_t ev_start = nullptr, ev_pro = nullptr, ev_end = nullptr;
   double t_loop_ms = 0, t_pass_ms = 0, t_pro_ms = 0;
   int passes_launched = 0, passes_done = 0;
+  int seeded_in_loop = 0;  // last run: the loop kernel generated u_0 itself (pass 0)
   int64_t dev_bytes = 0;
   std::string err;
 };
@@ -673,6 +675,7 @@ int fcm_set_option(fcm_plan* p, int32_t key, int64_t value) {
     case FCM_OPT_GRAPH: p->use_graph = value ? 1 : 0; return FCM_OK;
     case FCM_OPT_LOOP: p->use_loop = value ? 1 : 0; return FCM_OK;
     case FCM_OPT_PROFILE: p->profile = value ? 1 : 0; return FCM_OK;
+    case FCM_OPT_SEED_PASS: p->seed_pass = value ? 1 : 0; return FCM_OK;
     case FCM_OPT_L2:
       if (value < 0 || value > 2) return FCM_E_ARG;
       p->l2_mode = (int)value;
@@ -787,11 +790,16 @@ int fcm_run(fcm_plan* p, double m, double eps, int32_t max_iters, double* v_out,
   bool loop = single && p->use_loop && p->variant != 1 && s0.g.tiles_local > 0;
   const bool graph = !loop && single && p->use_graph;
   bool looped = false;
+  p->seeded_in_loop = 0;
   if (loop) {
     CK(cudaEventRecord(p->ev_start, s0.stream));
-    if ((rc = step(p, 0, eps, max_iters))) return rc;
+    // seeded start: pass 0 of the loop kernel (no prologue launch);
+    // uploaded start: the prologue kernel reads the AoS rows first
+    const bool seed_pass = p->init_src == 1 && p->seed_pass;
+    if (!seed_pass && (rc = step(p, 0, eps, max_iters))) return rc;
     CK(cudaEventRecord(p->ev_pro, s0.stream));
     PassArgs a = make_args(p, s0, 1, eps, max_iters);
+    a.seed_pass = seed_pass ? 1 : 0;
     if (p->profile) {
       const int passes = std::min(max_iters, 64);
       if (!p->prof) {
@@ -810,8 +818,10 @@ int fcm_run(fcm_plan* p, double m, double eps, int32_t max_iters, double* v_out,
       p->prof_grid = grid;
       p->passes_launched = 1;
       looped = true;
+      p->seeded_in_loop = seed_pass ? 1 : 0;
     } else if (e == cudaErrorCooperativeLaunchTooLarge || e == cudaErrorNotSupported) {
       cudaGetLastError();  // grid cannot be co-resident: host-driven passes below
+      if (seed_pass && (rc = step(p, 0, eps, max_iters))) return rc;
     } else {
       CK(e);
     }
@@ -942,7 +952,7 @@ int fcm_download(fcm_plan* p, double* u_out, int32_t* labels_out) {
 int fcm_last_timing(const fcm_plan* p, double* out, int32_t count) {
   if (!p || !out) return FCM_E_ARG;
   const double v[] = {p->t_loop_ms, p->t_pass_ms, p->t_pro_ms, (double)p->passes_launched,
-                      (double)p->passes_done};
+                      (double)p->passes_done, (double)p->seeded_in_loop};
   for (int i = 0; i < count && i < (int)(sizeof v / sizeof v[0]); ++i) out[i] = v[i];
   return FCM_OK;
 }

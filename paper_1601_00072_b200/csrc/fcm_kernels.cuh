@@ -386,6 +386,34 @@ __global__ void __launch_bounds__(kThreads) pass_kernel(PassArgs a) {
 // Builds u_0 (fp32 SoA, for delta_1) and the sums of u_0^m x / u_0^m that
 // give v_1, from either the seeded generator (bit-exact with
 // core.init_membership) or an uploaded fp64 AoS initial membership.
+// Seeded start for the 4 consecutive voxels i0..i0+3 of this rank (the same
+// thread -> voxel map as the streaming pass): u_0 rows bit-exact with
+// core.init_membership (init_row_state), w = u^m folded into acc in voxel
+// order, u_0 returned as fp32 for the plane stores.
+template <int C, int MODE>
+__device__ __forceinline__ void seed_quad(const PassArgs& a, const Powers& pw, int c, int64_t i0,
+                                          const double* xd, int64_t nvalid, float4* un, double* acc) {
+  constexpr int PM = (MODE == MODE_M2 || MODE == MODE_LUT2) ? MODE_M2 : MODE_GEN;
+  const uint64_t row_step = (uint64_t)c * kGamma;  // SplitMix64 state advance per voxel
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    double u[C];
+    init_row_state<C>(a.seed + (uint64_t)(a.g.voxel0 + i0 + q) * row_step, c, u);
+    const bool valid = q < nvalid;
+#pragma unroll
+    for (int j = 0; j < C; ++j) {
+      if (j < c) {
+        const double w = pow_m<PM>(u[j], pw);  // the reference's pow(u, m)
+        if (valid) {
+          acc[j] = fma(w, xd[q], acc[j]);
+          acc[C + j] += w;
+        }
+        f4set(un[j], q, (float)u[j]);
+      }
+    }
+  }
+}
+
 template <typename XT, int C, int MODE, bool FROM_SEED>
 __global__ void __launch_bounds__(kThreads, 2) prologue_kernel(PassArgs a) {
   __shared__ SmemRedT<2 * C + 2> sm;
@@ -393,9 +421,8 @@ __global__ void __launch_bounds__(kThreads, 2) prologue_kernel(PassArgs a) {
   if (blockIdx.x == 0 && threadIdx.x == 0) a.ctl->tile_next[(a.seq + 1) & 1] = 0u;
   const Powers pw = load_powers(a);
   const int c = C <= 8 ? C : a.c;
-  const uint64_t row_step = (uint64_t)c * kGamma;  // SplitMix64 state advance per voxel
   const int ntiles = a.g.tiles_local;
-  const XT* __restrict__ x = reinterpret_cast<const XT*>(a.x);
+  const int chunks = (1 << a.g.tile_shift) / (kThreads * kVec);
   for (;;) {
     if (threadIdx.x == 0) sm.tile = (int)atomicAdd(&a.ctl->tile_next[a.seq & 1], 1u);
     __syncthreads();
@@ -406,29 +433,38 @@ __global__ void __launch_bounds__(kThreads, 2) prologue_kernel(PassArgs a) {
 #pragma unroll
     for (int s = 0; s < 2 * C + 2; ++s) acc[s] = 0.0;
     const int64_t base = (int64_t)lt << a.g.tile_shift;
-    const int steps = (1 << a.g.tile_shift) / kThreads;
-    // one voxel per thread per step: consecutive threads -> consecutive
-    // voxels, so every plane store is a coalesced 128-byte warp write
-    for (int r = 0; r < steps; ++r) {
-      const int64_t i = base + (int64_t)r * kThreads + threadIdx.x;
-      if (i >= a.g.n_local) break;
-      const double xd = (double)x[i];
-      double u[C];
+    // 4 consecutive voxels per thread per 1024-voxel chunk, chunk by chunk:
+    // the TMA pass's map, so both give the same tile partials bit for bit
+    for (int ch = 0; ch < chunks; ++ch) {
+      const int64_t i0 = base + (int64_t)ch * (kThreads * kVec) + threadIdx.x * kVec;
+      const int64_t nvalid = a.g.n_local - i0;
+      if (nvalid <= 0) break;
+      double xd[4];
+      XLoad<XT>::load4(reinterpret_cast<const XT*>(a.x), i0, xd);  // x is padded to whole tiles
+      float4 un[C];
       if (FROM_SEED) {
-        init_row_state<C>(a.seed + (uint64_t)(a.g.voxel0 + i) * row_step, c, u);
+        seed_quad<C, MODE>(a, pw, c, i0, xd, nvalid, un, acc);
       } else {
 #pragma unroll
-        for (int j = 0; j < C; ++j) u[j] = j < c ? a.u0_aos[i * c + j] : 0.0;
-      }
+        for (int q = 0; q < 4; ++q) {
+          const bool valid = q < nvalid;
 #pragma unroll
-      for (int j = 0; j < C; ++j) {
-        if (j < c) {
-          const double w = pow_m<MODE>(u[j], pw);  // the reference's pow(u, m)
-          acc[j] = fma(w, xd, acc[j]);
-          acc[C + j] += w;
-          __stcg(a.u_nxt + j * a.g.plane + i, (float)u[j]);
+          for (int j = 0; j < C; ++j) {
+            if (j < c) {
+              const double u = valid ? a.u0_aos[(i0 + q) * c + j] : 0.0;
+              const double w = pow_m<MODE>(u, pw);
+              if (valid) {
+                acc[j] = fma(w, xd[q], acc[j]);
+                acc[C + j] += w;
+              }
+              f4set(un[j], q, (float)u);
+            }
+          }
         }
       }
+#pragma unroll
+      for (int j = 0; j < C; ++j)
+        if (j < c) __stcg(reinterpret_cast<float4*>(a.u_nxt + j * a.g.plane + i0), un[j]);
     }
     tile_finish<C>(a, lt, acc, sm, true);
     __syncthreads();

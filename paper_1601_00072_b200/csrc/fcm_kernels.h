@@ -34,6 +34,7 @@ struct PassArgs {
   int finalize_local;     // 1: the CTA completing the rank root finalizes (single-rank jobs)
   int keep_l2;            // 1: x + u fit in L2 -> evict_last loads/stores (next pass hits L2)
   double* l1_buf;         // loop kernel: level-1 node results [2][noct][nodes[1]][nf] (pass parity)
+  int seed_pass;          // loop kernel: 1 = run the seeded start as pass 0 (no prologue kernel)
   uint64_t* prof;         // loop-kernel timeline [prof_passes][grid][kProbeSlots] or null
   int prof_passes;
 };

@@ -318,7 +318,7 @@ __device__ __forceinline__ uint64_t global_ns() {
 // record (pass, CTA) -- 0 pass start, 1 producer done claiming, 2 consumers
 // done, 3 barrier released, 4 tiles claimed.
 __device__ __forceinline__ void probe(const PassArgs& a, unsigned it, int k, uint64_t v) {
-  if (a.prof && it <= (unsigned)a.prof_passes)
+  if (a.prof && it >= 1 && it <= (unsigned)a.prof_passes)
     a.prof[((uint64_t)(it - 1) * gridDim.x + blockIdx.x) * kProbeSlots + k] = v;
 }
 
@@ -328,7 +328,7 @@ __device__ __forceinline__ void probe(const PassArgs& a, unsigned it, int k, uin
 // ring, then post the end-of-pass marker.
 template <typename XT, int C, int MODE>
 __device__ __forceinline__ int tma_produce(const PassArgs& a, uint8_t* smem, Pipe& ps, unsigned* counter,
-                                           unsigned it = 0) {
+                                           unsigned it = 0, bool x_only = false) {
   using L = TmaLayout<XT, C, MODE>;
   constexpr int S = L::kStages;
   const uint32_t bar0 = smem_u32(smem + L::kBarOff);
@@ -361,7 +361,7 @@ __device__ __forceinline__ int tma_produce(const PassArgs& a, uint8_t* smem, Pip
       meta[ps.stage].chunk = ch;
       meta[ps.stage].last = ch == nch - 1;
       const uint32_t fb = bar0 + 8u * ps.stage;
-      mbar_arrive_tx(fb, (uint32_t)(L::kXBytes + c * L::kUBytes));
+      mbar_arrive_tx(fb, (uint32_t)(L::kXBytes + (x_only ? 0 : c * L::kUBytes)));
       const int64_t i0 = base + (int64_t)ch * kChunk;
       uint8_t* st = smem + ps.stage * L::kStageBytes;
       const void* xs = reinterpret_cast<const XT*>(a.x) + i0;
@@ -369,7 +369,7 @@ __device__ __forceinline__ int tma_produce(const PassArgs& a, uint8_t* smem, Pip
       else bulk_g2s(smem_u32(st), xs, L::kXBytes, fb);
 #pragma unroll
       for (int j = 0; j < C; ++j)
-        if (j < c) {
+        if (j < c && !x_only) {
           const uint32_t dst = smem_u32(st + L::kXBytes + j * L::kUBytes);
           const float* src = a.u_cur + j * a.g.plane + i0;
           if (keep) bulk_g2s_keep(dst, src, L::kUBytes, fb, pol);
@@ -444,6 +444,86 @@ __device__ __forceinline__ void tma_build_lut2(uint8_t* lut, const double* v) {
 // element is in the stage before the same thread overwrites it) and fold the
 // Eq. 3 / objective / delta terms; at the end of each tile run the fixed
 // reduction tree.  Returns after the end-of-pass marker.
+// Consumers of the loop kernel's seeded start (pass 0): the stage carries x
+// only; u_0 is generated per voxel (seed_quad: bit-exact SplitMix64 rows),
+// stored as the first fp32 membership and folded into Eq. 3's sums; tile
+// partials go to the reducer like any pass.  Same thread -> voxel map and
+// tree as prologue_kernel, so both starts give the same v_1 bit for bit.
+template <typename XT, int C, int MODE>
+__device__ __forceinline__ void tma_consume_seed(const PassArgs& a, uint8_t* smem, Pipe& ps,
+                                                 RedSlots<2 * C + 2>& rs, Pipe& sp, const Powers& pw) {
+  using L = TmaLayout<XT, C, MODE>;
+  constexpr int S = L::kStages;
+  constexpr int NS = 2 * C + 2;
+  const int tid = threadIdx.x;
+  const uint32_t bar0 = smem_u32(smem + L::kBarOff);
+  const StageMeta* meta = reinterpret_cast<const StageMeta*>(smem + L::kMetaOff);
+  const int64_t tile = int64_t(1) << a.g.tile_shift;
+  const int c = C <= 8 ? C : a.c;
+  const bool keep = a.keep_l2 != 0;
+  const uint64_t pol = keep ? l2_keep_policy() : 0ull;
+  double acc[NS];
+#pragma unroll
+  for (int s = 0; s < NS; ++s) acc[s] = 0.0;
+  for (;;) {
+    mbar_wait(bar0 + 8u * ps.stage, ps.phase);
+    const StageMeta mt = meta[ps.stage];
+    const uint8_t* st = smem + ps.stage * L::kStageBytes;
+    if (mt.tile < 0) {
+      __syncwarp();
+      if ((tid & 31) == 0) mbar_arrive(bar0 + 8u * (S + ps.stage));
+      ps.advance<S>();
+      mbar_wait(smem_u32(&rs.empty[sp.stage]), sp.phase ^ 1u);
+      if (tid == 0) rs.tile[sp.stage] = -1;
+      __syncwarp();
+      if ((tid & 31) == 0) mbar_arrive(smem_u32(&rs.full[sp.stage]));
+      sp.advance<kSlots>();
+      return;
+    }
+    const int64_t i0 = (int64_t)mt.tile * tile + (int64_t)mt.chunk * kChunk + tid * kVec;
+    double xd[4];
+    if (sizeof(XT) == 1) {
+      const uint32_t w = *reinterpret_cast<const uint32_t*>(st + tid * 4);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) xd[q] = u8_to_f64((w >> (8 * q)) & 0xffu);
+    } else {
+      const double2 p0 = *reinterpret_cast<const double2*>(st + tid * 32);
+      const double2 p1 = *reinterpret_cast<const double2*>(st + tid * 32 + 16);
+      xd[0] = p0.x;
+      xd[1] = p0.y;
+      xd[2] = p1.x;
+      xd[3] = p1.y;
+    }
+    __syncwarp();
+    if ((tid & 31) == 0) mbar_arrive(bar0 + 8u * (S + ps.stage));
+    ps.advance<S>();
+    float4 un[C];
+    seed_quad<C, MODE>(a, pw, c, i0, xd, a.g.n_local - i0, un, acc);
+#pragma unroll
+    for (int j = 0; j < C; ++j)
+      if (j < c) st_u4(reinterpret_cast<float4*>(a.u_nxt + j * a.g.plane + i0), un[j], keep, pol);
+    if (mt.last) {
+      double r[NS];
+#pragma unroll
+      for (int s2 = 0; s2 < NS; ++s2) r[s2] = warp_tree(acc[s2], s2 == NS - 1);
+      mbar_wait(smem_u32(&rs.empty[sp.stage]), sp.phase ^ 1u);
+      if ((tid & 31) == 0) {
+#pragma unroll
+        for (int s2 = 0; s2 < NS; ++s2) {
+          const int f = field_of<C>(s2, c);
+          if (f >= 0) rs.w[sp.stage][tid >> 5][f] = r[s2];
+        }
+        if (tid == 0) rs.tile[sp.stage] = mt.tile;
+      }
+      __syncwarp();
+      if ((tid & 31) == 0) mbar_arrive(smem_u32(&rs.full[sp.stage]));
+      sp.advance<kSlots>();
+#pragma unroll
+      for (int s = 0; s < NS; ++s) acc[s] = 0.0;
+    }
+  }
+}
+
 template <typename XT, int C, int MODE>
 __device__ __forceinline__ void tma_consume(const PassArgs& a, uint8_t* smem, Pipe& ps,
                                             RedSlots<2 * C + 2>& rs, Pipe& sp, const double* v,
@@ -938,6 +1018,26 @@ __device__ __forceinline__ bool grid_barrier(Control* ctl, unsigned it, unsigned
 __device__ __forceinline__ void finalize_loop(const PassArgs& a, const double* root, unsigned it, double* vsh,
                                               int* s_done) {
   const int c = a.c;
+  if (it == 0) {  // seeded start: v_1 or DegenerateClusterError (core.py:121-123)
+    int dead = -1;
+    for (int j = 0; j < c; ++j)
+      if (root[c + j] == 0.0) {
+        dead = j;
+        break;
+      }
+    if (dead < 0)
+      for (int j = 0; j < c; ++j) vsh[j] = root[j] / root[c + j];
+    *s_done = dead >= 0 ? 1 : 0;
+    if (blockIdx.x == 0) {
+      Control* ctl = a.ctl;
+      for (int f = 0; f < 2 * c + 2; ++f) ctl->root[f] = root[f];
+      ctl->dead = dead;
+      if (dead < 0)
+        for (int j = 0; j < c; ++j) ctl->v[j] = vsh[j];
+      ctl->done = dead >= 0 ? 1 : 0;
+    }
+    return;
+  }
   const int k = (int)it;
   const double delta = root[2 * c + 1];
   const bool conv = delta < a.eps;
@@ -998,14 +1098,15 @@ __global__ void __launch_bounds__(kTmaThreads, 2) loop_tma_kernel(PassArgs a) {
   const Powers pw = load_powers(a);
   const int64_t l1_len = (int64_t)a.g.noct * a.g.nodes[1] * (2 * a.c + 2);
   Pipe ps, sp;
+  unsigned gen = 0;  // grid-barrier generations
   __syncthreads();
-  for (unsigned it = 1; !s_done && it <= (unsigned)a.max_iters; ++it) {
+  for (unsigned it = a.seed_pass ? 0u : 1u; !s_done && it <= (unsigned)a.max_iters; ++it) {
     if (tid == 0) probe(a, it, 0, global_ns());
-    double* l1 = a.l1_buf + (it & 1) * l1_len;  // parity: readers of pass it-1 may still read the other half
+    double* l1 = a.l1_buf + (gen & 1) * l1_len;  // parity: readers of the last pass may still read the other half
     if (tid >= kThreads) {
       if (tid == kProducerTid) {
         fence_proxy_async_global();
-        const int n = tma_produce<XT, C, MODE>(a, smem, ps, &a.ctl->tile_next[1], it);  // zeroed by the prologue
+        const int n = tma_produce<XT, C, MODE>(a, smem, ps, &a.ctl->tile_next[1], it, it == 0);
         probe(a, it, 1, global_ns());
         probe(a, it, 4, (uint64_t)n);
         unsigned smid;
@@ -1015,6 +1116,8 @@ __global__ void __launch_bounds__(kTmaThreads, 2) loop_tma_kernel(PassArgs a) {
         tma_reduce<C, true>(a, rs, sp, &a.ctl->tile_next[1], l1, it);
         if ((tid & 31) == 0) probe(a, it, 7, global_ns());
       }
+    } else if (it == 0) {
+      tma_consume_seed<XT, C, MODE>(a, smem, ps, rs, sp, pw);
     } else {
       double v[C];
 #pragma unroll
@@ -1025,8 +1128,9 @@ __global__ void __launch_bounds__(kTmaThreads, 2) loop_tma_kernel(PassArgs a) {
       if (tid == 0) probe(a, it, 2, global_ns());
     }
     __syncthreads();
+    ++gen;  // every thread: gen selects the level-1 half below
     if (tid == 0) {
-      if (!grid_barrier(a.ctl, it, gridDim.x)) s_done = 1;
+      if (!grid_barrier(a.ctl, gen, gridDim.x)) s_done = 1;
       probe(a, it, 3, global_ns());
     }
     __syncthreads();

@@ -194,7 +194,7 @@ class FcmPlan:
         return buf[: passes.value * grid.value * 16].reshape(passes.value, grid.value, 16)
 
     def timing(self) -> dict:
-        keys = ("loop_ms", "pass_ms", "prologue_ms", "passes_launched", "passes")
+        keys = ("loop_ms", "pass_ms", "prologue_ms", "passes_launched", "passes", "seeded_in_loop")
         buf = (ctypes.c_double * len(keys))()
         check(lib().fcm_last_timing(self._h, buf, len(keys)), self._h, "fcm_last_timing")
         return dict(zip(keys, list(buf)))
