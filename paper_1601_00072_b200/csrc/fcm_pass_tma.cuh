@@ -209,22 +209,25 @@ __device__ __forceinline__ void voxel_general(double xd, const double* v, int c,
   }
 }
 
-// Per-pass intensity table for uint8 pixels (MODE_LUT): the Eq. 4 / Eq. 3
-// per-voxel terms are a function of the intensity alone, so each CTA
-// evaluates them once per pass for the 256 intensities (the same robust
-// fp64 formula the direct path uses, so values are identical) and the
-// stream then gathers them.  Rows are interleaved by 16-byte chunk
-// (chunk k of intensity b at (k*256 + b)*16) so lanes with different
-// intensities spread over the banks and equal intensities broadcast.
+// Per-pass intensity table for uint8 pixels (MODE_LUT, any m): Eq. 4 is a
+// function of the intensity alone, so each CTA evaluates the robust fp64
+// form once per pass for the 256 intensities.  The stream gathers u (fp32 +
+// fp32 residual, for the stores and an exact-to-1e-12 delta) and counts the
+// tile's intensities in per-warp shared-memory histograms; Eq. 3's sums and
+// the objective of a tile are then sum_b count_b * (w_b * b, w_b, J_b), with
+// thread b holding w_b = u_b^m and J_b in registers for the whole pass -- no
+// fp64 work per voxel.  Integer counts are exact, so a tile partial is a
+// pure function of the tile's intensity multiset.  Rows are interleaved by
+// 16-byte chunk (chunk k of intensity b at (k*256 + b)*16) so lanes with
+// different intensities spread over the banks and equal intensities
+// broadcast.  Histograms are double-buffered by tile parity.
 template <int C>
 struct LutLayout {
   static constexpr int K4 = (C + 3) / 4;  // float4 chunks of u (fp32) and of its residual
-  static constexpr int K2 = (C + 1) / 2;  // double2 chunks of w = u^m
   static constexpr int kUfOff = 0;
   static constexpr int kDuOff = kUfOff + K4 * 256 * 16;
-  static constexpr int kWOff = kDuOff + K4 * 256 * 16;
-  static constexpr int kJOff = kWOff + K2 * 256 * 16;
-  static constexpr int kBytes = kJOff + 256 * 8;
+  static constexpr int kHistOff = kDuOff + K4 * 256 * 16;  // uint32 [2][kWarps][256]
+  static constexpr int kBytes = kHistOff + 2 * kWarps * 256 * 4;
 };
 
 // m == 2 table (MODE_LUT2): per intensity the fp64 product-form memberships
@@ -383,8 +386,12 @@ __device__ __forceinline__ int tma_produce(const PassArgs& a, uint8_t* smem, Pip
 // ------------------------------------------------------- intensity table --
 // Entry b = tid: the same robust Eq. 4 evaluation as the direct path, so
 // table values equal per-voxel evaluation.  Ends with a consumer barrier.
+// Entry b = tid: the same robust Eq. 4 evaluation as the direct path.
+// Returns w_b * b, w_b and the objective term J_b (registers of thread b) and
+// clears thread b's histogram bins.  Ends with a consumer barrier.
 template <int C>
-__device__ __forceinline__ void tma_build_lut(uint8_t* lut, const double* v, int c, const Powers& pw) {
+__device__ __forceinline__ void tma_build_lut(uint8_t* lut, const double* v, int c, const Powers& pw,
+                                              double* wx, double* wb, double& jb) {
   using LL = LutLayout<C>;
   const int tid = threadIdx.x;
   const double xb = (double)tid;
@@ -392,20 +399,19 @@ __device__ __forceinline__ void tma_build_lut(uint8_t* lut, const double* v, int
   membership<C, MODE_GEN>(xb, v, c, pw, u);
   double jt = 0.0;
   float ufv[4 * LL::K4], duv[4 * LL::K4];
-  double wv[2 * LL::K2];
 #pragma unroll
   for (int j = 0; j < 4 * LL::K4; ++j) ufv[j] = duv[j] = 0.0f;
 #pragma unroll
-  for (int j = 0; j < 2 * LL::K2; ++j) wv[j] = 0.0;
-#pragma unroll
   for (int j = 0; j < C; ++j) {
-    const double w = pow_m<MODE_GEN>(u[j], pw);
+    const double w = j < c ? pow_m<MODE_GEN>(u[j], pw) : 0.0;
     const double d = xb - v[j];
     jt = fma(w, d * d, jt);
-    wv[j] = w;
+    wb[j] = w;
+    wx[j] = w * xb;
     ufv[j] = (float)u[j];
     duv[j] = (float)(u[j] - (double)ufv[j]);
   }
+  jb = jt;
 #pragma unroll
   for (int k = 0; k < LL::K4; ++k) {
     reinterpret_cast<float4*>(lut + LL::kUfOff)[k * 256 + tid] =
@@ -413,10 +419,9 @@ __device__ __forceinline__ void tma_build_lut(uint8_t* lut, const double* v, int
     reinterpret_cast<float4*>(lut + LL::kDuOff)[k * 256 + tid] =
         make_float4(duv[4 * k], duv[4 * k + 1], duv[4 * k + 2], duv[4 * k + 3]);
   }
+  uint32_t* hist = reinterpret_cast<uint32_t*>(lut + LL::kHistOff);
 #pragma unroll
-  for (int k = 0; k < LL::K2; ++k)
-    reinterpret_cast<double2*>(lut + LL::kWOff)[k * 256 + tid] = make_double2(wv[2 * k], wv[2 * k + 1]);
-  reinterpret_cast<double*>(lut + LL::kJOff)[tid] = jt;
+  for (int w = 0; w < 2 * kWarps; ++w) hist[w * 256 + tid] = 0u;
   red_sync<true>();
 }
 
@@ -527,7 +532,8 @@ __device__ __forceinline__ void tma_consume_seed(const PassArgs& a, uint8_t* sme
 template <typename XT, int C, int MODE>
 __device__ __forceinline__ void tma_consume(const PassArgs& a, uint8_t* smem, Pipe& ps,
                                             RedSlots<2 * C + 2>& rs, Pipe& sp, const double* v,
-                                            const Powers& pw) {
+                                            const Powers& pw, const double* lwx = nullptr,
+                                            const double* lwb = nullptr, double ljb = 0.0) {
   constexpr bool LUT = MODE == MODE_LUT;
   constexpr bool LUT2 = MODE == MODE_LUT2;
   using L = TmaLayout<XT, C, MODE>;
@@ -546,6 +552,8 @@ __device__ __forceinline__ void tma_consume(const PassArgs& a, uint8_t* smem, Pi
 #pragma unroll
   for (int s = 0; s < 2 * C + 2; ++s) acc[s] = 0.0;
   uint32_t dmax_hi = 0;
+  uint32_t* hist = reinterpret_cast<uint32_t*>(smem + L::kLutOff + (LUT ? LL::kHistOff : 0));
+  int hpar = 0;  // histogram buffer of the current tile
   for (;;) {
     mbar_wait(bar0 + 8u * ps.stage, ps.phase);
     const StageMeta mt = meta[ps.stage];
@@ -594,7 +602,6 @@ __device__ __forceinline__ void tma_consume(const PassArgs& a, uint8_t* smem, Pi
       if (LUT) {
         const int b = (int)(xd[q] - 0.0);
         float ufv[4 * LL::K4], duv[4 * LL::K4];
-        double wv[2 * LL::K2];
 #pragma unroll
         for (int k = 0; k < LL::K4; ++k) {
           const float4 f = reinterpret_cast<const float4*>(lut + LL::kUfOff)[k * 256 + b];
@@ -602,22 +609,12 @@ __device__ __forceinline__ void tma_consume(const PassArgs& a, uint8_t* smem, Pi
           ufv[4 * k] = f.x; ufv[4 * k + 1] = f.y; ufv[4 * k + 2] = f.z; ufv[4 * k + 3] = f.w;
           duv[4 * k] = e.x; duv[4 * k + 1] = e.y; duv[4 * k + 2] = e.z; duv[4 * k + 3] = e.w;
         }
-#pragma unroll
-        for (int k = 0; k < LL::K2; ++k) {
-          const double2 w2 = reinterpret_cast<const double2*>(lut + LL::kWOff)[k * 256 + b];
-          wv[2 * k] = w2.x;
-          wv[2 * k + 1] = w2.y;
-        }
-        if (valid) acc[2 * C] += reinterpret_cast<const double*>(lut + LL::kJOff)[b];
+        if (valid) atomicAdd(hist + (hpar * kWarps + (tid >> 5)) * 256 + b, 1u);
 #pragma unroll
         for (int j = 0; j < C; ++j) {
           // |u - u_old| = |(fl32(u) - u_old) + (u - fl32(u))|, both fp32-exact to ~1e-12
           const float dl = fabsf((ufv[j] - uq[j]) + duv[j]);
-          if (valid) {
-            acc[j] = fma(wv[j], xd[q], acc[j]);
-            acc[C + j] += wv[j];
-            dmax_f = fmaxf(dmax_f, dl);
-          }
+          if (valid) dmax_f = fmaxf(dmax_f, dl);
           nq[j] = ufv[j];
         }
       } else if (LUT2) {
@@ -642,6 +639,26 @@ __device__ __forceinline__ void tma_consume(const PassArgs& a, uint8_t* smem, Pi
     for (int j = 0; j < C; ++j)
       if (j < c) st_u4(reinterpret_cast<float4*>(a.u_nxt + j * a.g.plane + i0), un[j], keep, pol);
     if (mt.last) {
+      if (LUT) {
+        // every consumer warp has counted the tile: thread b folds bin b
+        // (exact count) into the tile's sums and clears it
+        red_sync<true>();
+        uint32_t cnt = 0;
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) {
+          uint32_t* h = hist + (hpar * kWarps + w) * 256 + tid;
+          cnt += *h;
+          *h = 0u;
+        }
+        const double cd = (double)cnt;
+#pragma unroll
+        for (int j = 0; j < C; ++j) {
+          acc[j] = cd * lwx[j];
+          acc[C + j] = cd * lwb[j];
+        }
+        acc[2 * C] = cd * ljb;
+        hpar ^= 1;
+      }
       acc[2 * C + 1] = LUT ? (double)dmax_f : __hiloint2double((int)dmax_hi, (int)0xffffffffu);
       // lanes -> warp value per field (adjacent-pair tree), then hand the
       // 8 warp values to the reducer through a slot
@@ -968,9 +985,10 @@ __global__ void __launch_bounds__(kTmaThreads, 2) pass_tma_kernel(PassArgs a) {
   double v[C];
   load_centers<C>(a.ctl, c, v);
   const Powers pw = load_powers(a);
-  if (LUT) tma_build_lut<C>(smem + L::kLutOff, v, c, pw);
+  double lwx[C], lwb[C], ljb = 0.0;
+  if (LUT) tma_build_lut<C>(smem + L::kLutOff, v, c, pw, lwx, lwb, ljb);
   if (MODE == MODE_LUT2) tma_build_lut2<C>(smem + L::kLutOff, v);
-  tma_consume<XT, C, MODE>(a, smem, ps, rs, sp, v, pw);
+  tma_consume<XT, C, MODE>(a, smem, ps, rs, sp, v, pw, lwx, lwb, ljb);
 }
 
 // -------------------------------------------------------- grid barrier ----
@@ -1122,9 +1140,10 @@ __global__ void __launch_bounds__(kTmaThreads, 2) loop_tma_kernel(PassArgs a) {
       double v[C];
 #pragma unroll
       for (int j = 0; j < C; ++j) v[j] = j < c ? vsh[j] : 0.0;
-      if (LUT) tma_build_lut<C>(smem + L::kLutOff, v, c, pw);
+      double lwx[C], lwb[C], ljb = 0.0;
+      if (LUT) tma_build_lut<C>(smem + L::kLutOff, v, c, pw, lwx, lwb, ljb);
       if (MODE == MODE_LUT2) tma_build_lut2<C>(smem + L::kLutOff, v);
-      tma_consume<XT, C, MODE>(a, smem, ps, rs, sp, v, pw);
+      tma_consume<XT, C, MODE>(a, smem, ps, rs, sp, v, pw, lwx, lwb, ljb);
       if (tid == 0) probe(a, it, 2, global_ns());
     }
     __syncthreads();
