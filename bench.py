@@ -11,9 +11,12 @@ buffers: pixel upload (uint8), solve, and download of the final membership
 (AoS float64) and labels.
 
 N > 1 (torchrun, one process per GPU): each rank owns a contiguous,
-tile-aligned voxel shard; the only per-iteration exchange is an
-ncclAllGather of the 2c+2 reduction roots (64 B at c=3) -- weak sharding of a
-fixed problem, reported as "strong" scaling (total work fixed).
+octant-aligned voxel shard of the fixed volume ("strong" scaling: total work
+fixed); the only per-iteration exchange is the 2c+2 reduction roots (64 B at
+c=3), written by each rank's loop kernel into every rank's mailbox over
+NVLink (--transport p2p, default; CUDA IPC handles gathered once with
+torch.distributed) or exchanged with one ncclAllGather per pass
+(--transport nccl).
 
 --impl reference runs the reference's own CPU engine (fcmseg from oracle/_ref,
 parallel._iterate on all host threads; the oracle port when oracle/_ref is
@@ -204,6 +207,14 @@ def run_ours(args, rank, world, local_rank, dist):
         dist.broadcast(buf, 0)
         nccl_id = bytes(buf.cpu().numpy().tobytes())
     plan = pkg.FcmPlan.for_rank(n, c, _lib.FCM_X_U8, local_rank, world, rank, nccl_id)
+    if world > 1 and args.transport == "p2p":
+        # fused exchange: map every rank's root mailbox (CUDA IPC over NVLink);
+        # the loop kernel then writes the 2c+2 roots straight into the peers
+        import torch
+        mine = torch.frombuffer(bytearray(plan.mailbox_handle()), dtype=torch.uint8).cuda()
+        allh = [torch.zeros_like(mine) for _ in range(world)]
+        dist.all_gather(allh, mine)
+        plan.connect_peers(b"".join(bytes(t.cpu().numpy().tobytes()) for t in allh), world)
     x = np.ascontiguousarray(x_full[plan.voxel0:plan.voxel0 + plan.n_local])
     del x_full
     plan.upload_pixels(x)
@@ -328,7 +339,9 @@ def run_ours(args, rank, world, local_rank, dist):
             "iterations_per_solve": iters[0],
             "step": "one fcm_run: device seeded start + fused passes to convergence",
             "l2": "inputs larger than L2 (x u8 + two fp32 SoA membership planes per iteration)",
-            "parallelism": f"voxel shards x{world}, ncclAllGather of 2c+2 roots per iteration"
+            "parallelism": (f"voxel shards x{world}, 2c+2 roots per iteration written into every rank's "
+                            f"mailbox by the loop kernel (NVLink peer stores)" if args.transport == "p2p" else
+                            f"voxel shards x{world}, ncclAllGather of 2c+2 roots per iteration")
             if world > 1 else "1 GPU",
         },
         "hbm_gbs_per_gpu": B * n / world * total_iters / (total_ms / 1e3) / 1e9,
@@ -414,6 +427,8 @@ def main():
     ap.add_argument("--config", default="C4", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
+                    help="N>1 root exchange: in-kernel peer-memory mailboxes (p2p) or ncclAllGather per pass")
     ap.add_argument("--no-seed-pass", action="store_true",
                     help="separate prologue kernel for the seeded start instead of the loop kernel's pass 0")
     ap.add_argument("--no-loop", action="store_true",

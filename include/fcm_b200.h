@@ -90,12 +90,24 @@ int fcm_plan_create(fcm_plan** out, int64_t n, int32_t c, int32_t x_kind, int32_
 
 /* One rank of an nranks-process job (one process per GPU): the plan owns the
  * rank's contiguous voxel range (query it with fcm_plan_info) and exchanges
- * the 2c+2 reduction roots with ncclAllGather.  nccl_id is the 128-byte
- * ncclUniqueId from fcm_nccl_unique_id on rank 0; NULL is allowed when nranks == 1
- * (a one-rank id still routes the roots through NCCL, which tests use). */
+ * the 2c+2 reduction roots with ncclAllGather, or -- after fcm_connect_peers --
+ * inside the loop kernel through peer-memory mailboxes.  nccl_id is the
+ * 128-byte ncclUniqueId from fcm_nccl_unique_id on rank 0, or NULL for a
+ * mailbox-only plan (a one-rank id still routes the roots through NCCL,
+ * which tests use). */
 int fcm_plan_create_rank(fcm_plan** out, int64_t n_global, int32_t c, int32_t x_kind,
                          int32_t device, int32_t nranks, int32_t rank, const void* nccl_id);
 int fcm_nccl_unique_id(void* out128);
+
+/* Multi-process ranks, fused exchange (loop kernel): the 64-byte CUDA IPC
+ * handle of this rank's rank-root mailbox, and the connection of a rank plan
+ * to every rank's mailbox (handles: nranks x 64 bytes, rank order, gathered
+ * by the caller, e.g. torch.distributed.all_gather).  Once connected, fcm_run
+ * runs the whole solve in one loop-kernel launch per rank and exchanges the
+ * 2c+2-double roots with NVLink peer stores inside the kernel instead of an
+ * ncclAllGather per pass. */
+int fcm_mailbox_handle(fcm_plan* plan, void* out64);
+int fcm_connect_peers(fcm_plan* plan, const void* handles, int32_t nranks);
 
 /* Host-only: the voxel range and reduction-tree geometry of `rank` in an
  * nranks job over n voxels (no GPU needed).  out[0..]: n_local, voxel0,

@@ -71,6 +71,7 @@ struct Shard {
   double* tile_part = nullptr;
   double* node_part[kMaxLevels + 1] = {};  // level l >= 1: [noct][nodes[l]][nf]
   double* l1_buf = nullptr;                // loop kernel: [2][noct][nodes[1]][nf]
+  Mailbox* mbox = nullptr;                 // loop kernel: rank-root mailbox (own allocation: IPC-exportable)
   double* rank_root = nullptr;  // [2][nf], double-buffered by pass parity
   double* gathered = nullptr;   // [nranks][nf] (NCCL)
   unsigned* node_cnt[kMaxLevels + 1] = {};
@@ -114,6 +115,10 @@ struct fcm_plan {
   int l2_mode = 1;  // 0 never keep x/u in L2, 1 when they fit (default), 2 always
   int profile = 0;  // record the loop kernel's per-CTA timeline
   int seed_pass = 1;  // loop kernel generates the seeded u_0 as its pass 0
+  unsigned run_counter = 0;  // fcm_run calls (mailbox tags); identical on every rank
+  bool p2p_ready = false;    // multi-process ranks: peer mailboxes mapped (fcm_connect_peers)
+  Mailbox* peer_mbox[kOctants] = {};
+  bool peer_opened[kOctants] = {};
   uint64_t* prof = nullptr;
   int prof_passes = 0, prof_grid = 0;
   bool capturing = false;
@@ -246,6 +251,8 @@ int setup_shard(fcm_plan* p, Shard& s) {
   if ((rc = dalloc(p, s, &s.rank_root, (size_t)2 * nf))) return rc;
   if ((rc = dalloc(p, s, &s.gathered, (size_t)p->nranks * nf))) return rc;
   if ((rc = dalloc(p, s, &s.l1_buf, (size_t)2 * s.g.noct * s.g.nodes[1] * nf))) return rc;
+  if ((rc = dalloc(p, s, &s.mbox, 1))) return rc;
+  CK(cudaMemsetAsync(s.mbox, 0, sizeof(Mailbox), s.stream));
   unsigned* cnt = nullptr;
   if ((rc = dalloc(p, s, &cnt, cnt_total))) return rc;
   s.cnt_total = cnt_total;
@@ -283,6 +290,8 @@ void release(fcm_plan* p) {
   if (p->host_ctl) cudaFreeHost(p->host_ctl);
   if (p->host_tmpl) cudaFreeHost(p->host_tmpl);
   drop_graph(p);
+  for (int r = 0; r < kOctants; ++r)
+    if (p->peer_opened[r]) cudaIpcCloseMemHandle(p->peer_mbox[r]);
   if (p->comm && g_nccl.ok) g_nccl.CommDestroy(p->comm);
 }
 
@@ -628,8 +637,9 @@ int fcm_plan_create_rank(fcm_plan** out, int64_t n_global, int32_t c, int32_t x_
   rank_geometry(p->sh[0].g, nranks, rank);
   int rc = common_setup(p);
   // nranks == 1 with an id still builds a (one-rank) communicator: the NCCL
-  // exchange path then runs end to end on a single GPU (tests).
-  if (!rc && (nranks > 1 || nccl_id)) {
+  // exchange path then runs end to end on a single GPU (tests).  nranks > 1
+  // without an id: a mailbox-only plan (fcm_connect_peers before fcm_run).
+  if (!rc && nccl_id) {
     if (!nccl_id || !load_nccl()) {
       rc = fail(p, FCM_E_NCCL, "NCCL unavailable (set FCM_NCCL_LIB) or no unique id");
     } else {
@@ -707,7 +717,7 @@ int fcm_plan_info(const fcm_plan* p, int64_t* info, int32_t count) {
 int fcm_upload_pixels(fcm_plan* p, const void* x) {
   if (check_plan(p) || !x) return FCM_E_ARG;
   const size_t xsz = p->xkind == XK_U8 ? 1 : 8;
-  const int64_t host0 = p->use_nccl ? p->sh[0].g.voxel0 : 0;
+  const int64_t host0 = p->nranks > p->nshards ? p->sh[0].g.voxel0 : 0;  // rank plans: host buffers hold the rank slice
   for (int i = 0; i < p->nshards; ++i) {
     Shard& s = p->sh[i];
     if (s.g.n_local == 0) continue;
@@ -732,7 +742,7 @@ int fcm_init_membership(fcm_plan* p, uint64_t seed) {
 
 int fcm_upload_membership(fcm_plan* p, const double* u0) {
   if (check_plan(p) || !u0) return FCM_E_ARG;
-  const int64_t host0 = p->use_nccl ? p->sh[0].g.voxel0 : 0;
+  const int64_t host0 = p->nranks > p->nshards ? p->sh[0].g.voxel0 : 0;  // rank plans: host buffers hold the rank slice
   for (int i = 0; i < p->nshards; ++i) {
     Shard& s = p->sh[i];
     if (s.g.n_local == 0) continue;
@@ -761,6 +771,8 @@ int fcm_run(fcm_plan* p, double m, double eps, int32_t max_iters, double* v_out,
   if (max_iters < 1) return fail(p, FCM_E_ARG, "max_iters must be >= 1");
   if (!p->x_ready) return fail(p, FCM_E_STATE, "fcm_upload_pixels has not been called");
   if (!p->init_src) return fail(p, FCM_E_STATE, "no initial membership (init or upload)");
+  if (p->nshards == 1 && p->nranks > 1 && !p->use_nccl && !p->p2p_ready)
+    return fail(p, FCM_E_STATE, "rank plan without NCCL: call fcm_connect_peers first");
   set_powers(p, m);
 
   Control tmpl;
@@ -787,7 +799,10 @@ int fcm_run(fcm_plan* p, double m, double eps, int32_t max_iters, double* v_out,
   p->passes_launched = 0;
   int rc = FCM_OK;
   const bool single = p->nshards == 1 && !p->use_nccl && !p->timing;
-  bool loop = single && p->use_loop && p->variant != 1 && s0.g.tiles_local > 0;
+  // loop kernel: single-process plans (mailboxes in process for >1 shard) or
+  // multi-process ranks whose peer mailboxes are mapped
+  bool loop = p->use_loop && !p->timing && p->variant != 1 && (!p->use_nccl || p->p2p_ready);
+  for (int i = 0; i < p->nshards; ++i) loop = loop && p->sh[i].g.tiles_local > 0;
   const bool graph = !loop && single && p->use_graph;
   bool looped = false;
   p->seeded_in_loop = 0;
@@ -797,29 +812,59 @@ int fcm_run(fcm_plan* p, double m, double eps, int32_t max_iters, double* v_out,
     // uploaded start: the prologue kernel reads the AoS rows first
     const bool seed_pass = p->init_src == 1 && p->seed_pass;
     if (!seed_pass && (rc = step(p, 0, eps, max_iters))) return rc;
-    CK(cudaEventRecord(p->ev_pro, s0.stream));
-    PassArgs a = make_args(p, s0, 1, eps, max_iters);
-    a.seed_pass = seed_pass ? 1 : 0;
-    if (p->profile) {
-      const int passes = std::min(max_iters, 64);
-      if (!p->prof) {
-        int rc2 = dalloc(p, s0, &p->prof, (size_t)64 * 2 * s0.sms * 4 * kProbeSlots);
-        if (rc2) return rc2;
-      }
-      CK(cudaMemsetAsync(p->prof, 0, sizeof(uint64_t) * 64 * 2 * s0.sms * 4 * kProbeSlots, s0.stream));
-      a.prof = p->prof;
-      a.prof_passes = passes;
-      p->prof_passes = passes;
+    for (int i = 1; i < p->nshards; ++i) {  // shards start together with shard 0
+      CK(cudaSetDevice(p->sh[i].device));
+      CK(cudaStreamWaitEvent(p->sh[i].stream, p->ev_start, 0));
     }
-    int grid = 0;
-    cudaError_t e = launch_loop(p->xkind, p->c, p->mode, a, s0.sms, s0.stream, &grid, p->variant, p->force_grid);
+    CK(cudaSetDevice(s0.device));
+    CK(cudaEventRecord(p->ev_pro, s0.stream));
+    const unsigned run = ++p->run_counter & 0xffffu;
+    cudaError_t e = cudaSuccess;
+    for (int i = 0; i < p->nshards && e == cudaSuccess; ++i) {
+      Shard& s = p->sh[i];
+      CK(cudaSetDevice(s.device));
+      PassArgs a = make_args(p, s, 1, eps, max_iters);
+      a.seed_pass = seed_pass ? 1 : 0;
+      a.mb_ranks = p->nranks;
+      a.mb_rank = p->nshards > 1 ? i : p->rank;
+      a.mb_run = run ? run : 1;
+      a.mbox_local = s.mbox;
+      for (int r = 0; r < p->nranks; ++r) a.mbox_peer[r] = p->nshards > 1 ? p->sh[r].mbox : p->peer_mbox[r];
+      a.finalize_local = 1;  // every rank finalizes from the exchanged global root
+      if (p->profile && i == 0) {
+        const int passes = std::min(max_iters, 64);
+        if (!p->prof) {
+          int rc2 = dalloc(p, s0, &p->prof, (size_t)64 * 2 * s0.sms * 4 * kProbeSlots);
+          if (rc2) return rc2;
+        }
+        CK(cudaMemsetAsync(p->prof, 0, sizeof(uint64_t) * 64 * 2 * s0.sms * 4 * kProbeSlots, s0.stream));
+        a.prof = p->prof;
+        a.prof_passes = passes;
+        p->prof_passes = passes;
+      }
+      // shards sharing a device split its SMs so every loop kernel is resident at once
+      int share = 0;
+      for (int j = 0; j < p->nshards; ++j) share += p->sh[j].device == s.device ? 1 : 0;
+      int grid = 0;
+      e = launch_loop(p->xkind, p->c, p->mode, a, s.sms, s.stream, &grid, p->variant, p->force_grid, share);
+      if (e == cudaSuccess) {
+        s.last_grid = grid;
+        if (i == 0) p->prof_grid = grid;
+      }
+    }
+    CK(cudaSetDevice(s0.device));
     if (e == cudaSuccess) {
-      s0.last_grid = grid;
-      p->prof_grid = grid;
       p->passes_launched = 1;
       looped = true;
       p->seeded_in_loop = seed_pass ? 1 : 0;
-    } else if (e == cudaErrorCooperativeLaunchTooLarge || e == cudaErrorNotSupported) {
+      for (int i = 1; i < p->nshards; ++i) {  // ev_end on shard 0 covers every shard
+        CK(cudaSetDevice(p->sh[i].device));
+        CK(cudaEventRecord(p->sh[i].ev_pass, p->sh[i].stream));
+        CK(cudaSetDevice(s0.device));
+        CK(cudaStreamWaitEvent(s0.stream, p->sh[i].ev_pass, 0));
+      }
+    } else if ((e == cudaErrorCooperativeLaunchTooLarge || e == cudaErrorNotSupported) && p->nshards == 1 &&
+               !p->use_nccl) {
       cudaGetLastError();  // grid cannot be co-resident: host-driven passes below
       if (seed_pass && (rc = step(p, 0, eps, max_iters))) return rc;
     } else {
@@ -912,7 +957,7 @@ int fcm_run(fcm_plan* p, double m, double eps, int32_t max_iters, double* v_out,
 int fcm_download(fcm_plan* p, double* u_out, int32_t* labels_out) {
   if (check_plan(p)) return FCM_E_ARG;
   if (!p->run_ok) return fail(p, FCM_E_STATE, "no successful fcm_run to download");
-  const int64_t host0 = p->use_nccl ? p->sh[0].g.voxel0 : 0;
+  const int64_t host0 = p->nranks > p->nshards ? p->sh[0].g.voxel0 : 0;  // rank plans: host buffers hold the rank slice
   for (int i = 0; i < p->nshards; ++i) {
     Shard& s = p->sh[i];
     if (s.g.n_local == 0) continue;
@@ -954,6 +999,38 @@ int fcm_last_timing(const fcm_plan* p, double* out, int32_t count) {
   const double v[] = {p->t_loop_ms, p->t_pass_ms, p->t_pro_ms, (double)p->passes_launched,
                       (double)p->passes_done, (double)p->seeded_in_loop};
   for (int i = 0; i < count && i < (int)(sizeof v / sizeof v[0]); ++i) out[i] = v[i];
+  return FCM_OK;
+}
+
+int fcm_mailbox_handle(fcm_plan* p, void* out64) {
+  if (check_plan(p) || !out64) return FCM_E_ARG;
+  if (p->nshards != 1) return fail(p, FCM_E_STATE, "mailbox handles belong to rank plans");
+  cudaIpcMemHandle_t h;
+  CK(cudaSetDevice(p->sh[0].device));
+  CK(cudaIpcGetMemHandle(&h, p->sh[0].mbox));
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  memcpy(out64, &h, sizeof h);
+  return FCM_OK;
+}
+
+int fcm_connect_peers(fcm_plan* p, const void* handles, int32_t nranks) {
+  if (check_plan(p) || !handles) return FCM_E_ARG;
+  if (p->nshards != 1 || nranks != p->nranks) return fail(p, FCM_E_ARG, "connect needs a rank plan of %d ranks", p->nranks);
+  CK(cudaSetDevice(p->sh[0].device));
+  for (int r = 0; r < nranks; ++r) {
+    if (r == p->rank) {
+      p->peer_mbox[r] = p->sh[0].mbox;
+      continue;
+    }
+    if (p->peer_opened[r]) continue;
+    cudaIpcMemHandle_t h;
+    memcpy(&h, (const char*)handles + 64 * r, sizeof h);
+    void* ptr = nullptr;
+    CK(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    p->peer_mbox[r] = (Mailbox*)ptr;
+    p->peer_opened[r] = true;
+  }
+  p->p2p_ready = true;
   return FCM_OK;
 }
 

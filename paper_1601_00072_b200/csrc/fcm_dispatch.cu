@@ -7,7 +7,7 @@ namespace fcm {
 
 #define FCM_EXTERN(C)                                                                                \
   extern template cudaError_t launch_pass_c<C>(int, int, const PassArgs&, int, cudaStream_t, int*, int, int); \
-  extern template cudaError_t launch_loop_c<C>(int, int, const PassArgs&, int, cudaStream_t, int*, int, int); \
+  extern template cudaError_t launch_loop_c<C>(int, int, const PassArgs&, int, cudaStream_t, int*, int, int, int); \
   extern template cudaError_t launch_prologue_c<C>(int, int, bool, const PassArgs&, int, cudaStream_t); \
   extern template cudaError_t launch_epilogue_c<C>(int, int, const EpilogueArgs&, int, cudaStream_t);
 FCM_EXTERN(2) FCM_EXTERN(3) FCM_EXTERN(4) FCM_EXTERN(5) FCM_EXTERN(6) FCM_EXTERN(7) FCM_EXTERN(8) FCM_EXTERN(16)
@@ -55,9 +55,9 @@ cudaError_t launch_pass(int xkind, int c, int mode, const PassArgs& a, int sms, 
 }
 
 cudaError_t launch_loop(int xkind, int c, int mode, const PassArgs& a, int sms, cudaStream_t st,
-                        int* grid_out, int variant, int force_grid) {
+                        int* grid_out, int variant, int force_grid, int share) {
   if (c < 2 || c > kCMaxSupported) return cudaErrorInvalidValue;
-#define CALL(C) launch_loop_c<C>(xkind, mode, a, sms, st, grid_out, variant, force_grid)
+#define CALL(C) launch_loop_c<C>(xkind, mode, a, sms, st, grid_out, variant, force_grid, share)
   FCM_SWITCH(CALL)
 #undef CALL
 }

@@ -559,20 +559,20 @@ cudaError_t launch_pass_c(int xkind, int mode, const PassArgs& a, int sms, cudaS
 
 template <int C>
 cudaError_t launch_loop_c(int xkind, int mode, const PassArgs& a, int sms, cudaStream_t st, int* grid_out,
-                          int variant, int force_grid) {
+                          int variant, int force_grid, int share) {
   constexpr int MD = C <= 8 ? MODE_M2 : MODE_GEN;
   const bool m2 = (mode == MODE_M2) && C <= 8;
   if (variant == 1) return cudaErrorNotSupported;  // the LDG kernel has no loop form
   if (xkind == XK_U8) {
     if (C <= 8 && variant != 3 && (variant == 2 || !m2))
-      return launch_loop_tma<uint8_t, C, (C <= 8 ? MODE_LUT : MODE_GEN)>(a, sms, st, grid_out, force_grid);
+      return launch_loop_tma<uint8_t, C, (C <= 8 ? MODE_LUT : MODE_GEN)>(a, sms, st, grid_out, force_grid, share);
     if (C <= 8 && m2 && variant == 0)
-      return launch_loop_tma<uint8_t, C, (C <= 8 ? MODE_LUT2 : MODE_GEN)>(a, sms, st, grid_out, force_grid);
-    return m2 ? launch_loop_tma<uint8_t, C, MD>(a, sms, st, grid_out, force_grid)
-              : launch_loop_tma<uint8_t, C, MODE_GEN>(a, sms, st, grid_out, force_grid);
+      return launch_loop_tma<uint8_t, C, (C <= 8 ? MODE_LUT2 : MODE_GEN)>(a, sms, st, grid_out, force_grid, share);
+    return m2 ? launch_loop_tma<uint8_t, C, MD>(a, sms, st, grid_out, force_grid, share)
+              : launch_loop_tma<uint8_t, C, MODE_GEN>(a, sms, st, grid_out, force_grid, share);
   }
-  return m2 ? launch_loop_tma<double, C, MD>(a, sms, st, grid_out, force_grid)
-            : launch_loop_tma<double, C, MODE_GEN>(a, sms, st, grid_out, force_grid);
+  return m2 ? launch_loop_tma<double, C, MD>(a, sms, st, grid_out, force_grid, share)
+            : launch_loop_tma<double, C, MODE_GEN>(a, sms, st, grid_out, force_grid, share);
 }
 
 template <int C>
@@ -609,7 +609,7 @@ cudaError_t launch_epilogue_c(int xkind, int mode, const EpilogueArgs& a, int sm
 
 #define FCM_INSTANTIATE(C)                                                                        \
   template cudaError_t launch_pass_c<C>(int, int, const PassArgs&, int, cudaStream_t, int*, int, int); \
-  template cudaError_t launch_loop_c<C>(int, int, const PassArgs&, int, cudaStream_t, int*, int, int); \
+  template cudaError_t launch_loop_c<C>(int, int, const PassArgs&, int, cudaStream_t, int*, int, int, int); \
   template cudaError_t launch_prologue_c<C>(int, int, bool, const PassArgs&, int, cudaStream_t); \
   template cudaError_t launch_epilogue_c<C>(int, int, const EpilogueArgs&, int, cudaStream_t);
 

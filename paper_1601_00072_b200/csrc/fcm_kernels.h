@@ -35,6 +35,11 @@ struct PassArgs {
   int keep_l2;            // 1: x + u fit in L2 -> evict_last loads/stores (next pass hits L2)
   double* l1_buf;         // loop kernel: level-1 node results [2][noct][nodes[1]][nf] (pass parity)
   int seed_pass;          // loop kernel: 1 = run the seeded start as pass 0 (no prologue kernel)
+  int mb_ranks;           // loop kernel: ranks exchanging roots through mailboxes (1 = none)
+  int mb_rank;            // this rank's slot
+  unsigned mb_run;        // run tag (fcm_run counter, identical on every rank)
+  Mailbox* mbox_local;              // this rank's mailbox (device memory of this rank)
+  Mailbox* mbox_peer[kOctants];     // every rank's mailbox as mapped here (peer / IPC pointers)
   uint64_t* prof;         // loop-kernel timeline [prof_passes][grid][kProbeSlots] or null
   int prof_passes;
 };
@@ -69,7 +74,7 @@ cudaError_t launch_pass(int xkind, int c, int mode, const PassArgs& a, int sms, 
 // Persistent loop kernel (all passes of a run in one cooperative launch);
 // returns cudaErrorCooperativeLaunchTooLarge when the grid cannot be resident.
 cudaError_t launch_loop(int xkind, int c, int mode, const PassArgs& a, int sms, cudaStream_t st,
-                        int* grid_out, int variant = 0, int force_grid = 0);
+                        int* grid_out, int variant = 0, int force_grid = 0, int share = 1);
 cudaError_t launch_prologue(int xkind, int c, int mode, bool from_seed, const PassArgs& a, int sms,
                             cudaStream_t st);
 cudaError_t launch_epilogue(int xkind, int c, int mode, const EpilogueArgs& a, int sms,

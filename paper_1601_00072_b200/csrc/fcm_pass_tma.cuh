@@ -311,6 +311,19 @@ __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
+__device__ __forceinline__ unsigned ld_acquire_sys_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ double ld_relaxed_sys(const double* p) {
+  double v;
+  asm volatile("ld.relaxed.sys.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ uint64_t global_ns() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -1088,6 +1101,50 @@ __device__ __forceinline__ void finalize_loop(const PassArgs& a, const double* r
   }
 }
 
+// Loop kernel, multi-rank: publish this rank's root (in root[], every CTA
+// has it) to every rank's mailbox, wait for all ranks' roots of this pass in
+// the local mailbox, and replace root[] by the rank-ordered pair tree over
+// them -- the same tree the octants use (tree_model.combine_ranks), so the
+// global root is the single-rank root bit for bit.  All threads call it.
+// Returns false on a 4 s timeout (a peer died): the run is flagged.
+__device__ __forceinline__ bool exchange_roots(const PassArgs& a, double* root, unsigned gen) {
+  const int tid = threadIdx.x;
+  const int nf = 2 * a.c + 2;
+  const int par = gen & 1;
+  const unsigned tag = (a.mb_run << 16) | (gen & 0xffffu);
+  if (blockIdx.x == 0 && tid < a.mb_ranks) {  // thread p writes rank p's copy (NVLink stores)
+    Mailbox* mb = a.mbox_peer[tid];
+    for (int f = 0; f < nf; ++f) mb->root[par][a.mb_rank][f] = root[f];
+    __threadfence_system();
+    st_release_sys_u32(&mb->tag[par][a.mb_rank], tag);
+  }
+  __shared__ int s_ok;
+  if (tid == 0) {
+    s_ok = 1;
+    const uint64_t t0 = global_ns();
+    for (int r = 0; r < a.mb_ranks && s_ok; ++r)
+      while (ld_acquire_sys_u32(&a.mbox_local->tag[par][r]) != tag) {
+        __nanosleep(64);
+        if (global_ns() - t0 > 4000000000ull) {
+          s_ok = 0;
+          break;
+        }
+      }
+  }
+  __syncthreads();
+  if (!s_ok) return false;
+  for (int f = tid; f < nf; f += kTmaThreads) {
+    double v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = i < a.mb_ranks ? ld_relaxed_sys(&a.mbox_local->root[par][i][f]) : 0.0;
+    const bool mx = f == nf - 1;
+    root[f] = combine(combine(combine(v[0], v[1], mx), combine(v[2], v[3], mx), mx),
+                      combine(combine(v[4], v[5], mx), combine(v[6], v[7], mx), mx), mx);
+  }
+  __syncthreads();
+  return true;
+}
+
 // --------------------------------------------- persistent loop kernel -----
 // The whole device loop of core._iterate (core.py:118-131) in ONE launch:
 // every CTA stays resident (cooperative launch), runs pass after pass over
@@ -1155,6 +1212,13 @@ __global__ void __launch_bounds__(kTmaThreads, 2) loop_tma_kernel(PassArgs a) {
     __syncthreads();
     if (s_done) break;
     loop_upper<NF>(a, l1, reinterpret_cast<double*>(smem), oroot, rs.root);
+    if (a.mb_ranks > 1 && !exchange_roots(a, rs.root, gen)) {
+      if (tid == 0) {
+        a.ctl->dead = -3;
+        a.ctl->done = 1;
+      }
+      break;
+    }
     if (tid == 0) {
       finalize_loop(a, rs.root, it, vsh, &s_done);
       probe(a, it, 14, global_ns());
@@ -1191,7 +1255,7 @@ inline cudaError_t launch_pass_tma(const PassArgs& a, int sms, cudaStream_t st, 
 // launch (fails instead of deadlocking when the grid cannot be co-resident).
 template <typename XT, int C, int MODE>
 inline cudaError_t launch_loop_tma(const PassArgs& a, int sms, cudaStream_t st, int* grid_out,
-                                   int force_grid) {
+                                   int force_grid, int share = 1) {
   using L = TmaLayout<XT, C, MODE>;
   auto k = loop_tma_kernel<XT, C, MODE>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kSmemBytes);
@@ -1200,7 +1264,7 @@ inline cudaError_t launch_loop_tma(const PassArgs& a, int sms, cudaStream_t st, 
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kTmaThreads, L::kSmemBytes);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorCooperativeLaunchTooLarge;
-  long long g = (long long)per_sm * sms;
+  long long g = (long long)per_sm * sms / (share > 0 ? share : 1);
   if (force_grid > 0 && force_grid < g) g = force_grid;
   if (g > a.g.tiles_local) g = a.g.tiles_local;
   if (g < 1) g = 1;

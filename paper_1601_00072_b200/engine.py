@@ -107,6 +107,18 @@ class FcmPlan:
                                          int(nranks), int(rank), idbuf), None, "fcm_plan_create_rank")
         return cls(n_global, c, x_kind, _handle=h)
 
+    def mailbox_handle(self) -> bytes:
+        """64-byte CUDA IPC handle of this rank's root mailbox (fused exchange)."""
+        buf = ctypes.create_string_buffer(64)
+        check(lib().fcm_mailbox_handle(self._h, buf), self._h, "fcm_mailbox_handle")
+        return buf.raw
+
+    def connect_peers(self, handles: bytes, nranks: int):
+        """Map every rank's mailbox (handles of all ranks, rank order): the loop kernel then
+        exchanges the per-pass roots with NVLink peer stores instead of NCCL."""
+        buf = ctypes.create_string_buffer(bytes(handles), 64 * nranks)
+        check(lib().fcm_connect_peers(self._h, buf, int(nranks)), self._h, "fcm_connect_peers")
+
     @staticmethod
     def nccl_unique_id() -> bytes:
         FcmPlan._locate_nccl()

@@ -296,3 +296,30 @@ def test_three_level_tree_loop_vs_per_pass_vs_shards_bitwise():
         assert ka == kb and ca == cb
         assert va.tobytes() == vb.tobytes() and ta.tobytes() == tb.tobytes()
         assert ua.tobytes() == ub.tobytes() and np.array_equal(la, lb)
+
+
+@pytest.mark.parametrize("devices", [[0, 0], [0] * 8])
+@pytest.mark.parametrize("c,m", [(3, 2.0), (8, 1.5)])
+def test_mailbox_exchange_loop_kernels_bitwise(devices, c, m):
+    """N loop kernels running side by side on one B200 (one per shard),
+    exchanging their rank roots through peer-memory mailboxes every pass:
+    the same bits as one kernel over the whole volume."""
+    from paper_1601_00072_b200 import _lib
+    x = np.clip(np.rint(mixture_pixels(1_000_003, c, seed=5 + c)), 0, 255).astype(np.uint8)
+
+    def solve(devs):
+        plan = pkg.FcmPlan(x.shape[0], c, _lib.FCM_X_U8, devices=devs) if devs else pkg.FcmPlan(x.shape[0], c, _lib.FCM_X_U8)
+        with plan:
+            plan.upload_pixels(x)
+            plan.init_membership(11)
+            out = plan.run(m, 1e-5, 200)
+            t = plan.timing()
+            u, lab = plan.download()
+        return out, u, lab, t
+
+    (va, ta, ka, ca), ua, la, _ = solve(None)
+    (vb, tb, kb, cb), ub, lb, tm = solve(devices)
+    assert tm["passes_launched"] == 1  # the fused loop kernels ran the whole solve
+    assert ka == kb and ca == cb
+    assert va.tobytes() == vb.tobytes() and ta.tobytes() == tb.tobytes()
+    assert ua.tobytes() == ub.tobytes() and np.array_equal(la, lb)

@@ -1,0 +1,70 @@
+"""Two processes, one mailbox-connected rank plan each (CUDA IPC), on one GPU or two.
+
+    python tools/ipc_two_ranks.py [--same-gpu]
+
+Each rank owns its octant range of the volume; roots are exchanged by the
+loop kernels through each other's mailboxes.  Rank 0 compares the result with
+a single-process solve bit for bit.  (On one GPU the two cooperative kernels
+time-share the device; the in-kernel exchange has a 4 s timeout.)
+"""
+import os
+import sys
+
+import numpy as np
+import torch.multiprocessing as mp
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def worker(rank, world, port, same_gpu, out):
+    sys.path.insert(0, REPO)
+    sys.path.insert(0, os.path.join(REPO, "tests"))
+    import torch
+    import torch.distributed as dist
+    import paper_1601_00072_b200 as pkg
+    from paper_1601_00072_b200 import _lib
+    from conftest import mixture_pixels
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    n = 300_007
+    x = np.clip(np.rint(mixture_pixels(n, 3, seed=9)), 0, 255).astype(np.uint8)
+    dev = 0 if same_gpu else rank
+    plan = pkg.FcmPlan.for_rank(n, 3, _lib.FCM_X_U8, dev, world, rank, None)
+    plan.upload_pixels(x[plan.voxel0:plan.voxel0 + plan.n_local])
+    plan.init_membership(4)
+    mine = torch.frombuffer(bytearray(plan.mailbox_handle()), dtype=torch.uint8)
+    allh = [torch.zeros_like(mine) for _ in range(world)]
+    dist.all_gather(allh, mine)
+    plan.connect_peers(b"".join(bytes(t.numpy().tobytes()) for t in allh), world)
+    dist.barrier()
+    v, trace, k, conv = plan.run(2.0, 1e-5, 100)
+    u, lab = plan.download()
+    parts = [None] * world
+    dist.all_gather_object(parts, (plan.voxel0, u.tobytes(), lab.tobytes()))
+    if rank == 0:
+        with pkg.FcmPlan(n, 3, _lib.FCM_X_U8, devices=[0]) as ref:
+            ref.upload_pixels(x)
+            ref.init_membership(4)
+            rv, rt, rk, rc = ref.run(2.0, 1e-5, 100)
+            ru, rl = ref.download()
+        u_all = b"".join(p[1] for p in sorted(parts))
+        l_all = b"".join(p[2] for p in sorted(parts))
+        ok = (rk == k and v.tobytes() == rv.tobytes() and trace.tobytes() == rt.tobytes()
+              and u_all == ru.tobytes() and l_all == rl.tobytes())
+        with open(out, "w") as f:
+            f.write(f"{'OK' if ok else 'MISMATCH'} iters={k} v={v}\n")
+    plan.close()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    import socket
+    same = "--same-gpu" in sys.argv
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    out = os.path.join(REPO, "gpurun_out", "ipc_two_ranks.txt")
+    mp.spawn(worker, args=(2, port, same, out), nprocs=2, join=True)
+    print(open(out).read())
