@@ -54,6 +54,13 @@ def algorithmic_bytes(c: int) -> int:
     return 1 + 8 * c
 
 
+def _device_count():
+    import ctypes
+    from paper_1601_00072_b200 import _lib
+    n = ctypes.c_int32()
+    return n.value if _lib.lib().fcm_device_count(ctypes.byref(n)) == 0 else 1
+
+
 def load_peaks():
     try:
         with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
@@ -198,20 +205,25 @@ def run_ours(args, rank, world, local_rank, dist):
     max_iters = 500
     x_full = make_volume(shape)
 
+    # collectives of the harness itself (ids, handles, timing maxima): on the
+    # GPU with NCCL, or on host tensors when the process group is gloo
+    # (FCM_BENCH_DIST_BACKEND=gloo, used to run N ranks on one test GPU)
+    tdev = "cuda" if (world > 1 and dist.get_backend() == "nccl") else "cpu"
+    device = local_rank % max(1, _device_count()) if os.environ.get("FCM_BENCH_DEVICE_MODULO") else local_rank
     nccl_id = None
-    if world > 1:
+    if world > 1 and args.transport == "nccl":
         import torch
-        buf = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        buf = torch.zeros(128, dtype=torch.uint8, device=tdev)
         if rank == 0:
             buf.copy_(torch.frombuffer(bytearray(pkg.FcmPlan.nccl_unique_id()), dtype=torch.uint8))
         dist.broadcast(buf, 0)
         nccl_id = bytes(buf.cpu().numpy().tobytes())
-    plan = pkg.FcmPlan.for_rank(n, c, _lib.FCM_X_U8, local_rank, world, rank, nccl_id)
+    plan = pkg.FcmPlan.for_rank(n, c, _lib.FCM_X_U8, device, world, rank, nccl_id)
     if world > 1 and args.transport == "p2p":
         # fused exchange: map every rank's root mailbox (CUDA IPC over NVLink);
         # the loop kernel then writes the 2c+2 roots straight into the peers
         import torch
-        mine = torch.frombuffer(bytearray(plan.mailbox_handle()), dtype=torch.uint8).cuda()
+        mine = torch.frombuffer(bytearray(plan.mailbox_handle()), dtype=torch.uint8).to(tdev)
         allh = [torch.zeros_like(mine) for _ in range(world)]
         dist.all_gather(allh, mine)
         plan.connect_peers(b"".join(bytes(t.cpu().numpy().tobytes()) for t in allh), world)
@@ -231,7 +243,7 @@ def run_ours(args, rank, world, local_rank, dist):
         if world == 1:
             return v
         import torch
-        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        t = torch.tensor([v], dtype=torch.float64, device=tdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -242,7 +254,7 @@ def run_ours(args, rank, world, local_rank, dist):
     # graph (prologue + device-side while loop); CUDA events around it.
     barrier()
     loop_ms, iters, launched, kern_ms = [], [], [], []
-    with ClockSampler(local_rank) as clk:
+    with ClockSampler(device) as clk:
         t_wall = time.perf_counter()
         for _ in range(args.steps):
             v, trace, k, conv = plan.run(m, eps, max_iters)
@@ -262,14 +274,16 @@ def run_ours(args, rank, world, local_rank, dist):
 
     # ---- per-pass kernel timing (A/B): the same solves launched pass by pass
     # with CUDA events around every pass kernel on the launching stream
-    plan.set_option(_lib.FCM_OPT_TIMING, 1)
-    pass_ms, pro_ms = [], []
-    for _ in range(max(2, min(args.steps, 5))):
-        plan.run(m, eps, max_iters)
-        t = plan.timing()
-        pass_ms.append(t["pass_ms"])
-        pro_ms.append(t["prologue_ms"])
-    plan.set_option(_lib.FCM_OPT_TIMING, 0)
+    pass_ms, pro_ms = [0.0], [0.0]
+    if world == 1 or args.transport == "nccl":  # mailbox-only rank plans have no per-pass mode
+        plan.set_option(_lib.FCM_OPT_TIMING, 1)
+        pass_ms, pro_ms = [], []
+        for _ in range(max(2, min(args.steps, 5))):
+            plan.run(m, eps, max_iters)
+            t = plan.timing()
+            pass_ms.append(t["pass_ms"])
+            pro_ms.append(t["prologue_ms"])
+        plan.set_option(_lib.FCM_OPT_TIMING, 0)
     pass_avg = max_over_ranks(float(np.mean(pass_ms)))
 
     # ---- e2e: host buffers through the C ABI (upload, solve, download)
@@ -338,7 +352,9 @@ def run_ours(args, rank, world, local_rank, dist):
             "n_voxels": n, "c": c, "m": m, "epsilon": eps, "seed": 0,
             "iterations_per_solve": iters[0],
             "step": "one fcm_run: device seeded start + fused passes to convergence",
-            "l2": "inputs larger than L2 (x u8 + two fp32 SoA membership planes per iteration)",
+            "l2": ("inputs larger than L2 (x u8 + the c fp32 membership planes, 3.4 GB per pass at C4); no flush needed"
+                   if n * (1 + 4 * c) > 126e6 else
+                   "working set (x + memberships) fits L2 and is kept there between passes (evict_last policy); not flushed"),
             "parallelism": (f"voxel shards x{world}, 2c+2 roots per iteration written into every rank's "
                             f"mailbox by the loop kernel (NVLink peer stores)" if args.transport == "p2p" else
                             f"voxel shards x{world}, ncclAllGather of 2c+2 roots per iteration")
@@ -450,8 +466,10 @@ def main():
         if world > 1:
             import torch
             import torch.distributed as dist
-            torch.cuda.set_device(local_rank)
-            dist.init_process_group("nccl")
+            backend = os.environ.get("FCM_BENCH_DIST_BACKEND", "nccl")
+            if backend == "nccl":
+                torch.cuda.set_device(local_rank)
+            dist.init_process_group(backend)
         out = run_ours(args, rank, world, local_rank, dist)
         if dist is not None:
             dist.barrier()

@@ -804,6 +804,8 @@ int fcm_run(fcm_plan* p, double m, double eps, int32_t max_iters, double* v_out,
   bool loop = p->use_loop && !p->timing && p->variant != 1 && (!p->use_nccl || p->p2p_ready);
   for (int i = 0; i < p->nshards; ++i) loop = loop && p->sh[i].g.tiles_local > 0;
   const bool graph = !loop && single && p->use_graph;
+  if (!loop && p->nranks > p->nshards && !p->use_nccl)
+    return fail(p, FCM_E_STATE, "a mailbox-only rank plan runs the loop kernel only (no NCCL for per-pass launches)");
   bool looped = false;
   p->seeded_in_loop = 0;
   if (loop) {
