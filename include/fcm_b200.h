@@ -152,6 +152,15 @@ int fcm_run(fcm_plan* plan, double m, double epsilon, int32_t max_iters, double*
  * of the plan's voxel range.  Either pointer may be NULL. */
 int fcm_download(fcm_plan* plan, double* u_aos_out, int32_t* labels_out);
 
+/* Label statistics of the last solve, counted on the device from the labels
+ * fcm_download left there (metrics.py:46-97: Dice and match_clusters need
+ * only these integers).  ref_labels: int32 class per voxel of the plan's
+ * range in [0, c_ref); conf_out[p*c_ref + r] = |pred==p & ref==r|.
+ * mask: one byte per voxel (nonzero = set); counts_out[0..c) = |pred==p &
+ * mask|, counts_out[c] = |mask|, counts_out[c+1+p] = |pred==p|. */
+int fcm_label_confusion(fcm_plan* plan, const int32_t* ref_labels, int32_t c_ref, int64_t* conf_out);
+int fcm_mask_overlap(fcm_plan* plan, const uint8_t* mask, int64_t* counts_out);
+
 /* out[0..]: ms of the last fcm_run's device loop (start + passes, CUDA
  * events), ms per pass (FCM_OPT_TIMING: mean pass-kernel time; loop kernel:
  * its duration / passes, the seeded start included), prologue-kernel ms

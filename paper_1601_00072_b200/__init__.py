@@ -26,7 +26,11 @@ from .engine import (
     update_centers,
     update_membership,
 )
-from .errors import DegenerateClusterError, DeviceError, DimensionMismatchError, FcmError, InvalidConfigError
+from .errors import (DegenerateClusterError, DeviceError, DimensionMismatchError, FcmError, InvalidConfigError,
+                     MalformedHeaderError, MissingClassError, PgmError, PgmValueError, TruncatedRasterError,
+                     UnsupportedMagicError)
+from .imgio import PgmImage, label_intensity, parse_pgm, read_ground_truth, read_pgm, read_pgm_raster, write_pgm
+from .metrics import BinaryMask, DscReport, dsc, dsc_report_gpu, mask_for_class, match_clusters, match_clusters_gpu
 from .types import ROW_SUM_TOL, ClusterCenters, FcmConfig, FcmResult, GrayImage, LabelMap, MembershipMatrix
 
 __version__ = "0.1.0"
@@ -36,4 +40,8 @@ __all__ = [
     "objective", "pixel_kind", "run_fcm_gpu", "update_centers", "update_membership",
     "DegenerateClusterError", "DeviceError", "DimensionMismatchError", "FcmError", "InvalidConfigError",
     "ROW_SUM_TOL", "ClusterCenters", "FcmConfig", "FcmResult", "GrayImage", "LabelMap", "MembershipMatrix",
+    "MalformedHeaderError", "MissingClassError", "PgmError", "PgmValueError", "TruncatedRasterError",
+    "UnsupportedMagicError", "PgmImage", "label_intensity", "parse_pgm", "read_ground_truth", "read_pgm",
+    "read_pgm_raster", "write_pgm", "BinaryMask", "DscReport", "dsc", "dsc_report_gpu", "mask_for_class",
+    "match_clusters", "match_clusters_gpu",
 ]

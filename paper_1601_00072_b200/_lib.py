@@ -29,6 +29,8 @@ SIGNATURES = {
     "fcm_plan_create_rank": ([ctypes.POINTER(ctypes.c_void_p), ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
                               ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p], ctypes.c_int),
     "fcm_nccl_unique_id": ([ctypes.c_void_p], ctypes.c_int),
+    "fcm_label_confusion": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p], ctypes.c_int),
+    "fcm_mask_overlap": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
     "fcm_mailbox_handle": ([ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
     "fcm_connect_peers": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32], ctypes.c_int),
     "fcm_geometry": ([ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(ctypes.c_int64),

@@ -1004,6 +1004,53 @@ int fcm_last_timing(const fcm_plan* p, double* out, int32_t count) {
   return FCM_OK;
 }
 
+// Label statistics of the last solve on the device (metrics.py:46-97 counts).
+static int label_stats(fcm_plan* p, const int32_t* ref, int32_t cref, const uint8_t* mask, int64_t* out,
+                       int nbins) {
+  if (check_plan(p) || !out) return FCM_E_ARG;
+  if (!p->run_ok) return fail(p, FCM_E_STATE, "no successful fcm_run");
+  const int64_t host0 = p->nranks > p->nshards ? p->sh[0].g.voxel0 : 0;
+  std::vector<unsigned long long> total(nbins, 0ull), part(nbins);
+  for (int i = 0; i < p->nshards; ++i) {
+    Shard& s = p->sh[i];
+    if (s.g.n_local == 0) continue;
+    if (!s.out_labels) return fail(p, FCM_E_STATE, "download the labels (fcm_download) first");
+    CK(cudaSetDevice(s.device));
+    int32_t* dref = nullptr;
+    uint8_t* dmask = nullptr;
+    unsigned long long* dbins = nullptr;
+    CK(cudaMallocAsync(&dbins, sizeof(unsigned long long) * nbins, s.stream));
+    CK(cudaMemsetAsync(dbins, 0, sizeof(unsigned long long) * nbins, s.stream));
+    if (ref) {
+      CK(cudaMallocAsync(&dref, sizeof(int32_t) * s.g.n_local, s.stream));
+      CK(cudaMemcpyAsync(dref, ref + (s.g.voxel0 - host0), sizeof(int32_t) * s.g.n_local, cudaMemcpyHostToDevice,
+                         s.stream));
+    } else {
+      CK(cudaMallocAsync(&dmask, s.g.n_local, s.stream));
+      CK(cudaMemcpyAsync(dmask, mask + (s.g.voxel0 - host0), s.g.n_local, cudaMemcpyHostToDevice, s.stream));
+    }
+    CK(op_label_counts(s.out_labels, dref, dmask, s.g.n_local, p->c, cref, dbins, s.stream));
+    CK(cudaMemcpyAsync(part.data(), dbins, sizeof(unsigned long long) * nbins, cudaMemcpyDeviceToHost, s.stream));
+    if (dref) CK(cudaFreeAsync(dref, s.stream));
+    if (dmask) CK(cudaFreeAsync(dmask, s.stream));
+    CK(cudaFreeAsync(dbins, s.stream));
+    CK(cudaStreamSynchronize(s.stream));
+    for (int b = 0; b < nbins; ++b) total[b] += part[b];
+  }
+  for (int b = 0; b < nbins; ++b) out[b] = (int64_t)total[b];
+  return FCM_OK;
+}
+
+int fcm_label_confusion(fcm_plan* p, const int32_t* ref_labels, int32_t c_ref, int64_t* conf_out) {
+  if (check_plan(p) || !ref_labels || c_ref < 1 || c_ref > kCMaxSupported) return FCM_E_ARG;
+  return label_stats(p, ref_labels, c_ref, nullptr, conf_out, p->c * c_ref);
+}
+
+int fcm_mask_overlap(fcm_plan* p, const uint8_t* mask, int64_t* counts_out) {
+  if (check_plan(p) || !mask) return FCM_E_ARG;
+  return label_stats(p, nullptr, 0, mask, counts_out, 2 * p->c + 1);
+}
+
 int fcm_mailbox_handle(fcm_plan* p, void* out64) {
   if (check_plan(p) || !out64) return FCM_E_ARG;
   if (p->nshards != 1) return fail(p, FCM_E_STATE, "mailbox handles belong to rank plans");

@@ -4,6 +4,8 @@
 // (objective_linear), :211-220 (max_abs_diff), :223-238 (argmax_rows).
 // Sums use a fixed two-level tree (per-CTA chunk tree, then one CTA over the
 // partials) so every result is deterministic.
+#include <algorithm>
+
 #include "fcm_device.cuh"
 #include "fcm_ops.h"
 
@@ -110,6 +112,39 @@ cudaError_t op_reduce(int kind, const double* x, const double* u, const double* 
 
 cudaError_t op_argmax(const double* u, int32_t* labels, int64_t n, int c, cudaStream_t st) {
   argmax_kernel<<<grid_for(n), kThreads, 0, st>>>(u, labels, n, c);
+  return cudaGetLastError();
+}
+
+// Integer label statistics: shared-memory bins per
+// CTA, one 64-bit global atomic per bin per CTA.  Counts are exact.
+__global__ void label_counts_kernel(const int32_t* pred, const int32_t* ref, const uint8_t* mask, int64_t n,
+                                    int c, int cref, unsigned long long* bins) {
+  __shared__ unsigned sb[kCMaxSupported * kCMaxSupported + 2 * kCMaxSupported + 1];
+  const int nb = ref ? c * cref : 2 * c + 1;
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) sb[b] = 0u;
+  __syncthreads();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int p = pred[i];
+    if (ref) {
+      atomicAdd(&sb[p * cref + ref[i]], 1u);
+    } else {
+      atomicAdd(&sb[c + 1 + p], 1u);
+      if (mask[i]) {
+        atomicAdd(&sb[p], 1u);
+        atomicAdd(&sb[c], 1u);
+      }
+    }
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < nb; b += blockDim.x)
+    if (sb[b]) atomicAdd(&bins[b], (unsigned long long)sb[b]);
+}
+
+cudaError_t op_label_counts(const int32_t* pred, const int32_t* ref, const uint8_t* mask, int64_t n, int c,
+                            int cref, unsigned long long* bins, cudaStream_t st) {
+  int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
+  if (grid < 1) grid = 1;
+  label_counts_kernel<<<grid, 256, 0, st>>>(pred, ref, mask, n, c, cref, bins);
   return cudaGetLastError();
 }
 

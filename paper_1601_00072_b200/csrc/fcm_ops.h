@@ -11,4 +11,8 @@ cudaError_t op_reduce(int kind, const double* x, const double* u, const double* 
                       double m, const double* a, const double* b, double* scratch, double* out,
                       cudaStream_t st);
 cudaError_t op_argmax(const double* u, int32_t* labels, int64_t n, int c, cudaStream_t st);
+// Label statistics of a solve (metrics): bins[p*cref + r] += |pred==p & ref==r| when ref is set;
+// bins[p] += |pred==p & mask|, bins[c] += |mask|, bins[c+1+p] += |pred==p| when mask is set.
+cudaError_t op_label_counts(const int32_t* pred, const int32_t* ref, const uint8_t* mask, int64_t n, int c,
+                            int cref, unsigned long long* bins, cudaStream_t st);
 }  // namespace fcm

@@ -205,6 +205,35 @@ class FcmPlan:
               self._h, "fcm_last_profile")
         return buf[: passes.value * grid.value * 16].reshape(passes.value, grid.value, 16)
 
+    # -- label statistics (metrics on the device) ------------------------
+    def confusion(self, ref_labels: np.ndarray, c_ref: int) -> np.ndarray:
+        """[c, c_ref] counts |pred==p & ref==r| of the last solve's labels (after download)."""
+        ref = np.ascontiguousarray(ref_labels, dtype=np.int32)
+        if ref.shape[0] != self.n_local:
+            raise DimensionMismatchError(f"reference labels cover {ref.shape[0]} voxels, expected {self.n_local}")
+        if ref.size and (ref.min() < 0 or ref.max() >= c_ref):
+            raise InvalidConfigError(f"reference labels must lie in [0, {c_ref})")
+        out = np.zeros(self.c * c_ref, dtype=np.int64)
+        check(lib().fcm_label_confusion(self._h, ptr(ref), int(c_ref), ptr(out)), self._h, "fcm_label_confusion")
+        return out.reshape(self.c, c_ref)
+
+    def _mask_stats(self, mask) -> np.ndarray:
+        m = np.ascontiguousarray(np.asarray(mask, dtype=bool)).view(np.uint8)
+        if m.shape[0] != self.n_local:
+            raise DimensionMismatchError(f"mask covers {m.shape[0]} voxels, expected {self.n_local}")
+        out = np.zeros(2 * self.c + 1, dtype=np.int64)
+        check(lib().fcm_mask_overlap(self._h, ptr(m), ptr(out)), self._h, "fcm_mask_overlap")
+        return out
+
+    def mask_overlap(self, mask):
+        """(|pred==p & mask| for each cluster p, |mask|) for the last solve's labels."""
+        st = self._mask_stats(mask)
+        return st[: self.c], int(st[self.c])
+
+    def label_counts(self) -> np.ndarray:
+        """|pred==p| for each cluster p."""
+        return self._mask_stats(np.zeros(self.n_local, dtype=bool))[self.c + 1:]
+
     def timing(self) -> dict:
         keys = ("loop_ms", "pass_ms", "prologue_ms", "passes_launched", "passes", "seeded_in_loop")
         buf = (ctypes.c_double * len(keys))()
@@ -240,8 +269,13 @@ def _iterate(x: np.ndarray, u0: np.ndarray | None, cfg: FcmConfig, devices=None,
 
 
 def run_fcm_gpu(img: GrayImage, cfg: FcmConfig, devices=None,
-                initial_membership: MembershipMatrix | None = None) -> FcmResult:
+                initial_membership: MembershipMatrix | None = None, keep_plan: bool = False):
     """Cluster an image on the GPU; drop-in for run_fcm_sequential / run_fcm_parallel.
+
+    `img` is a GrayImage or an imgio.PgmImage (integer raster, no float64
+    expansion).  keep_plan=True returns (FcmResult, FcmPlan) with the plan's
+    labels still resident for the device-side metrics (metrics.dsc_report_gpu);
+    the caller closes the plan.
 
     Same seeded initialization as the reference engines (SplitMix64, generated
     on the device), same convergence rule, same result contract.  `devices`
@@ -255,8 +289,12 @@ def run_fcm_gpu(img: GrayImage, cfg: FcmConfig, devices=None,
     if initial_membership is not None and (initial_membership.n != n or initial_membership.c != cfg.c):
         raise DimensionMismatchError(
             f"initial membership is {initial_membership.n}x{initial_membership.c}, expected {n}x{cfg.c}")
-    kind, xx = pixel_kind(img.pixels)
-    with FcmPlan(n, cfg.c, kind, devices) as plan:
+    # a PgmImage (imgio.read_pgm_raster) hands its integer raster over as is:
+    # 8-bit images reach HBM at 1 B per voxel without a float64 copy
+    from .imgio import PgmImage
+    kind, xx = pixel_kind(img.raster if isinstance(img, PgmImage) else img.pixels)
+    plan = FcmPlan(n, cfg.c, kind, devices)
+    try:
         plan.upload_pixels(xx)
         if initial_membership is None:
             plan.init_membership(cfg.seed64)
@@ -264,7 +302,12 @@ def run_fcm_gpu(img: GrayImage, cfg: FcmConfig, devices=None,
             plan.upload_membership(initial_membership.u)
         v, trace, k, conv = plan.run(cfg.m, cfg.epsilon, cfg.max_iters)
         u, labels = plan.download()
-    return FcmResult(
+    except BaseException:
+        plan.close()
+        raise
+    if not keep_plan:
+        plan.close()
+    result = FcmResult(
         centers=ClusterCenters(v),
         membership=MembershipMatrix(n, cfg.c, u),
         labels=LabelMap(img.width, img.height, labels, cfg.c),
@@ -272,6 +315,7 @@ def run_fcm_gpu(img: GrayImage, cfg: FcmConfig, devices=None,
         objective_trace=tuple(float(t) for t in trace),
         converged=conv,
     )
+    return (result, plan) if keep_plan else result
 
 
 ENGINES = {"gpu": run_fcm_gpu}
