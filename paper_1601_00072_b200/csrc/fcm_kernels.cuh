@@ -415,7 +415,7 @@ __device__ __forceinline__ void seed_quad(const PassArgs& a, const Powers& pw, i
 }
 
 template <typename XT, int C, int MODE, bool FROM_SEED>
-__global__ void __launch_bounds__(kThreads, 4) prologue_kernel(PassArgs a) {
+__global__ void __launch_bounds__(kThreads, C <= 4 ? 4 : 2) prologue_kernel(PassArgs a) {
   __shared__ SmemRedT<2 * C + 2> sm;
   if (pass_done(a, sm)) return;
   if (blockIdx.x == 0 && threadIdx.x == 0) a.ctl->tile_next[(a.seq + 1) & 1] = 0u;
