@@ -710,17 +710,14 @@ __device__ __forceinline__ bool try_node(double* child0, int nreal, int nf, doub
   const int lane = threadIdx.x & 31;
   const bool real = lane < nreal;
   double* src = child0 + (int64_t)lane * nf;
-  bool ok = !real || !is_sentinel(ld_relaxed(src + nf - 1));
-  if (!__all_sync(0xffffffffu, ok)) return false;
+  // one round trip: every field of every child in flight at once, then check
   double v[NF];
 #pragma unroll
-  for (int f = 0; f < NF; ++f) {
-    v[f] = 0.0;
-    if (f < nf && real) {
-      v[f] = ld_relaxed(src + f);
-      ok = ok && !is_sentinel(v[f]);
-    }
-  }
+  for (int f = 0; f < NF; ++f) v[f] = (f < nf && real) ? ld_relaxed(src + f) : 0.0;
+  bool ok = true;
+#pragma unroll
+  for (int f = 0; f < NF; ++f)
+    if (f < nf && real) ok = ok && !is_sentinel(v[f]);
   if (!__all_sync(0xffffffffu, ok)) return false;
 #pragma unroll
   for (int f = 0; f < NF; ++f)
@@ -851,7 +848,7 @@ __device__ __forceinline__ void tma_reduce(const PassArgs& a, RedSlots<2 * C + 2
       backoff = 64;
     } else if (slots_done) {
       __nanosleep(backoff);  // pass drained: poll the pending node with a short backoff
-      backoff = min(backoff * 2, 512u);
+      backoff = min(backoff * 2, 128u);
     }
   }
   if (!LOOP && cta0) {
@@ -896,7 +893,7 @@ __device__ __forceinline__ double tree32(const double* p, int64_t stride, int nr
 // tree32; all kTmaThreads threads call it; scratch is the (idle) stage ring.
 template <int NF>
 __device__ __forceinline__ void loop_upper(const PassArgs& a, const double* l1, double* scratch,
-                                           double (*oroot)[NF], double* root) {
+                                           double (*oroot)[NF], double* root, unsigned it = 0) {
   const int tid = threadIdx.x;
   const int nf = 2 * a.c + 2;
   const Geometry& g = a.g;
@@ -912,6 +909,7 @@ __device__ __forceinline__ void loop_upper(const PassArgs& a, const double* l1, 
       scratch[(int64_t)item * NF + f] = nreal ? tree32<true>(src, nf, nreal, f == nf - 1) : 0.0;
     }
     __syncthreads();
+    if (tid == 0) probe(a, it, 11, global_ns());
   }
   // step 2: octant roots
   for (int pr = tid; pr < g.noct * nf; pr += kTmaThreads) {
@@ -1047,7 +1045,7 @@ __device__ __forceinline__ bool grid_barrier(Control* ctl, unsigned it, unsigned
 // DegenerateClusterError(j), else v_{k+1}) on the CTA's own copy; CTA 0 also
 // publishes them to the control block and the trace.
 __device__ __forceinline__ void finalize_loop(const PassArgs& a, const double* root, unsigned it, double* vsh,
-                                              int* s_done) {
+                                              const double* vnew, int* s_done) {
   const int c = a.c;
   if (it == 0) {  // seeded start: v_1 or DegenerateClusterError (core.py:121-123)
     int dead = -1;
@@ -1057,7 +1055,7 @@ __device__ __forceinline__ void finalize_loop(const PassArgs& a, const double* r
         break;
       }
     if (dead < 0)
-      for (int j = 0; j < c; ++j) vsh[j] = root[j] / root[c + j];
+      for (int j = 0; j < c; ++j) vsh[j] = vnew[j];  // root[j] / root[c + j]
     *s_done = dead >= 0 ? 1 : 0;
     if (blockIdx.x == 0) {
       Control* ctl = a.ctl;
@@ -1082,7 +1080,7 @@ __device__ __forceinline__ void finalize_loop(const PassArgs& a, const double* r
         break;
       }
   if (!done)
-    for (int j = 0; j < c; ++j) vsh[j] = root[j] / root[c + j];
+    for (int j = 0; j < c; ++j) vsh[j] = vnew[j];  // root[j] / root[c + j], computed side by side
   *s_done = done ? 1 : 0;
   if (blockIdx.x == 0) {
     Control* ctl = a.ctl;
@@ -1162,6 +1160,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) loop_tma_kernel(PassArgs a) {
   __shared__ RedSlots<NF> rs;
   __shared__ double oroot[kOctants][NF];
   __shared__ double vsh[C];
+  __shared__ double vnew[C];
   __shared__ int s_done;
   const int tid = threadIdx.x;
   const int c = C <= 8 ? C : a.c;
@@ -1211,7 +1210,8 @@ __global__ void __launch_bounds__(kTmaThreads, 2) loop_tma_kernel(PassArgs a) {
     }
     __syncthreads();
     if (s_done) break;
-    loop_upper<NF>(a, l1, reinterpret_cast<double*>(smem), oroot, rs.root);
+    loop_upper<NF>(a, l1, reinterpret_cast<double*>(smem), oroot, rs.root, it);
+    if (tid == 0) probe(a, it, 10, global_ns());
     if (a.mb_ranks > 1 && !exchange_roots(a, rs.root, gen)) {
       if (tid == 0) {
         a.ctl->dead = -3;
@@ -1219,8 +1219,10 @@ __global__ void __launch_bounds__(kTmaThreads, 2) loop_tma_kernel(PassArgs a) {
       }
       break;
     }
+    if (tid < c) vnew[tid] = rs.root[tid] / rs.root[c + tid];  // the c divisions side by side
+    __syncthreads();
     if (tid == 0) {
-      finalize_loop(a, rs.root, it, vsh, &s_done);
+      finalize_loop(a, rs.root, it, vsh, vnew, &s_done);
       probe(a, it, 14, global_ns());
     }
     __syncthreads();

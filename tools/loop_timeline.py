@@ -59,3 +59,8 @@ b0 = int(P[1, :, 0].min())
 print("consumers done max", (int(P[1, :, 2].max()) - b0) / 1e3, "reducers done max", (int(P[1, :, 7].max()) - b0) / 1e3,
       "barrier released", (int(P[1, :, 3].max()) - b0) / 1e3, "root done max", (int(P[1, :, 14].max()) - b0) / 1e3,
       "next start max", (int(P[2, :, 0].max()) - b0) / 1e3)
+
+def mx(j, it=1):
+    return (int(P[it, :, j].max()) - int(P[it, :, 0].min())) / 1e3
+print("pass 2 chain (max over CTAs, us from pass start): consumers", mx(2), "reducers", mx(7), "barrier", mx(3),
+      "upper step1", mx(11), "upper done", mx(10), "finalize", mx(14), "next start", (int(P[2, :, 0].max()) - int(P[1, :, 0].min())) / 1e3)
