@@ -734,7 +734,7 @@ __device__ __forceinline__ bool try_node(double* child0, int nreal, int nf, doub
 
 template <int NF, bool GLOBAL_OUT>
 __device__ __forceinline__ void wait_node(double* child0, int nreal, int nf, double* out) {
-  while (!try_node<NF, GLOBAL_OUT>(child0, nreal, nf, out)) __nanosleep(128);
+  while (!try_node<NF, GLOBAL_OUT>(child0, nreal, nf, out)) __nanosleep(32);
 }
 
 // Node k of CTA 0's upper-level list -- levels 2..L, octant by octant, each
