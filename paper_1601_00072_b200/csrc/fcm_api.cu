@@ -70,7 +70,7 @@ struct Shard {
   double* u0_aos = nullptr;
   double* tile_part = nullptr;
   double* node_part[kMaxLevels + 1] = {};  // level l >= 1: [noct][nodes[l]][nf]
-  double* l1_buf = nullptr;                // loop kernel: [2][noct][nodes[1]][nf]
+  double* l1_buf = nullptr;                // loop kernel: [3][noct][nodes[1]][nf] (pass generation mod 3)
   Mailbox* mbox = nullptr;                 // loop kernel: rank-root mailbox (own allocation: IPC-exportable)
   double* rank_root = nullptr;  // [2][nf], double-buffered by pass parity
   double* gathered = nullptr;   // [nranks][nf] (NCCL)
@@ -250,7 +250,7 @@ int setup_shard(fcm_plan* p, Shard& s) {
   }
   if ((rc = dalloc(p, s, &s.rank_root, (size_t)2 * nf))) return rc;
   if ((rc = dalloc(p, s, &s.gathered, (size_t)p->nranks * nf))) return rc;
-  if ((rc = dalloc(p, s, &s.l1_buf, (size_t)2 * s.g.noct * s.g.nodes[1] * nf))) return rc;
+  if ((rc = dalloc(p, s, &s.l1_buf, (size_t)3 * s.g.noct * s.g.nodes[1] * nf))) return rc;
   if ((rc = dalloc(p, s, &s.mbox, 1))) return rc;
   CK(cudaMemsetAsync(s.mbox, 0, sizeof(Mailbox), s.stream));
   unsigned* cnt = nullptr;
@@ -793,6 +793,7 @@ int fcm_run(fcm_plan* p, double m, double eps, int32_t max_iters, double* v_out,
     CK(cudaMemsetAsync(s.tile_part, 0xff, sizeof(double) * std::max(s.g.tiles_local, 1) * nf, s.stream));
     for (int l = 1; l <= s.g.levels; ++l)
       CK(cudaMemsetAsync(s.node_part[l], 0xff, sizeof(double) * s.g.noct * s.g.nodes[l] * nf, s.stream));
+    CK(cudaMemsetAsync(s.l1_buf, 0xff, sizeof(double) * 3 * s.g.noct * s.g.nodes[1] * nf, s.stream));
   }
   Shard& s0 = p->sh[0];
   CK(cudaSetDevice(s0.device));

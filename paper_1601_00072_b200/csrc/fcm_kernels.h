@@ -33,7 +33,7 @@ struct PassArgs {
   int use_cond;
   int finalize_local;     // 1: the CTA completing the rank root finalizes (single-rank jobs)
   int keep_l2;            // 1: x + u fit in L2 -> evict_last loads/stores (next pass hits L2)
-  double* l1_buf;         // loop kernel: level-1 node results [2][noct][nodes[1]][nf] (pass parity)
+  double* l1_buf;         // loop kernel: level-1 node results [3][noct][nodes[1]][nf] (generation mod 3)
   int seed_pass;          // loop kernel: 1 = run the seeded start as pass 0 (no prologue kernel)
   int mb_ranks;           // loop kernel: ranks exchanging roots through mailboxes (1 = none)
   int mb_rank;            // this rank's slot

@@ -305,6 +305,16 @@ __device__ __forceinline__ void st_u4(float4* p, float4 v, bool keep, uint64_t p
   else
     __stcs(p, v);
 }
+// Pass-end barrier of the loop kernel (named barrier 2 over the whole CTA):
+// producer and consumers wait on it, the reducer warp only arrives (then
+// goes on reducing its level-1 nodes while thread 0 is in the grid barrier).
+__device__ __forceinline__ void bar_sync_end() {
+  asm volatile("bar.sync 2, %0;" ::"n"(kTmaThreads) : "memory");
+}
+__device__ __forceinline__ void bar_arrive_end() {
+  asm volatile("bar.arrive 2, %0;" ::"n"(kTmaThreads) : "memory");
+}
+
 // Orders this thread's generic-proxy view (u_k written by other CTAs, made
 // visible by the grid barrier) before its following TMA (async-proxy) reads.
 __device__ __forceinline__ void fence_proxy_async_global() {
@@ -788,6 +798,7 @@ __device__ __forceinline__ void tma_reduce(const PassArgs& a, RedSlots<2 * C + 2
   int zb = 0;
   bool slots_done = false;
   uint64_t n_poll = 0, n_node = 0;
+
   uint32_t backoff = 64;
   while (!slots_done || za < NA || zb < NB) {
     // next slot: sleep in hardware until it fills (bounded while a node is
@@ -811,6 +822,7 @@ __device__ __forceinline__ void tma_reduce(const PassArgs& a, RedSlots<2 * C + 2
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(&rs.empty[sp.stage]));
       sp.advance<kSlots>();
+      if (LOOP && slots_done) bar_arrive_end();  // the CTA may enter the grid barrier now
       continue;
     }
     int l, lo, j;
@@ -831,12 +843,19 @@ __device__ __forceinline__ void tma_reduce(const PassArgs& a, RedSlots<2 * C + 2
       const long long r0 = octant_real_nodes(g, oct, 0);
       const long long last = min(((long long)j + 1) << (5 * l), r0) - 1;
       const int last_lt = (int)((long long)oct * g.M - g.tile0 + last);
-      if ((int)ld_relaxed_u32(counter) > last_lt) {
+      // (loop kernel, after this CTA's slots: the barrier may already have
+      // re-armed the scheduler, so poll without the hand-out check)
+      if ((LOOP && slots_done) || (int)ld_relaxed_u32(counter) > last_lt) {
         ++n_poll;
         double* child0 = l == 1 ? a.tile_part + ((int64_t)oct * g.M - g.tile0 + (int64_t)j * kFan) * nf
                                 : a.node_part[l - 1] + ((int64_t)lo * g.nodes[l - 1] + (int64_t)j * kFan) * nf;
-        if (LOOP)
+        if (LOOP) {  // publish, then count it (readers wait for the count after the grid barrier)
           advance = try_node<NF, false>(child0, nreal, nf, l1_out + ((int64_t)lo * g.nodes[1] + j) * nf);
+          if (advance && lane == 0) {
+            __threadfence();
+            atomicAdd(&a.ctl->l1_done, 1u);
+          }
+        }
         else
           advance = try_node<NF, true>(child0, nreal, nf, a.node_part[l] + ((int64_t)lo * g.nodes[l] + j) * nf);
         n_node += advance;
@@ -879,6 +898,7 @@ __device__ __forceinline__ double tree32(const double* p, int64_t stride, int nr
 #pragma unroll
   for (int i = 0; i < 32; ++i)
     v[i] = i < nreal ? (GLOBAL ? __ldcg(p + (int64_t)i * stride) : p[(int64_t)i * stride]) : 0.0;
+
 #pragma unroll
   for (int s2 = 1; s2 < 32; s2 <<= 1)
 #pragma unroll
@@ -1040,6 +1060,17 @@ __device__ __forceinline__ bool grid_barrier(Control* ctl, unsigned it, unsigned
   return true;
 }
 
+// Wait (thread 0) until a monotone device counter reaches `target`; false on
+// a 4 s timeout (flags the run like a stuck grid barrier).
+__device__ __forceinline__ bool wait_count(unsigned* ctr, unsigned target) {
+  const uint64_t t0 = global_ns();
+  while (ld_acquire_u32(ctr) < target) {
+    __nanosleep(32);
+    if (global_ns() - t0 > 4000000000ull) return false;
+  }
+  return true;
+}
+
 // Loop kernel, thread 0 of every CTA after the redundant root of pass `it`:
 // the same decisions as finalize_body (core.py:120-131: converged, max_iters,
 // DegenerateClusterError(j), else v_{k+1}) on the CTA's own copy; CTA 0 also
@@ -1170,13 +1201,19 @@ __global__ void __launch_bounds__(kTmaThreads, 2) loop_tma_kernel(PassArgs a) {
     for (int j = 0; j < c; ++j) vsh[j] = __ldcg(&a.ctl->v[j]);
   }
   const Powers pw = load_powers(a);
-  const int64_t l1_len = (int64_t)a.g.noct * a.g.nodes[1] * (2 * a.c + 2);
+  const int64_t l1_len = (int64_t)a.g.noct * a.g.nodes[1] * (2 * a.c + 2);  // one of 3 buffers
+  unsigned l1_real = 0;  // real level-1 nodes of this rank (published once per pass)
+  for (int lo = 0; lo < a.g.noct; ++lo) l1_real += (unsigned)octant_real_nodes(a.g, a.g.oct0 + lo, 1);
   Pipe ps, sp;
   unsigned gen = 0;  // grid-barrier generations
   __syncthreads();
   for (unsigned it = a.seed_pass ? 0u : 1u; !s_done && it <= (unsigned)a.max_iters; ++it) {
     if (tid == 0) probe(a, it, 0, global_ns());
-    double* l1 = a.l1_buf + (gen & 1) * l1_len;  // parity: readers of the last pass may still read the other half
+    // level-1 results of this pass: buffer (gen+1) % 3; owners publish them
+    // after their CTA has entered the grid barrier and count them in
+    // ctl->l1_done (fence + atomic per node); readers wait for the count
+    const unsigned gnext = gen + 1;
+    double* l1 = a.l1_buf + (gnext % 3) * l1_len;
     if (tid >= kThreads) {
       if (tid == kProducerTid) {
         fence_proxy_async_global();
@@ -1186,26 +1223,37 @@ __global__ void __launch_bounds__(kTmaThreads, 2) loop_tma_kernel(PassArgs a) {
         unsigned smid;
         asm("mov.u32 %0, %%smid;" : "=r"(smid));
         probe(a, it, 6, smid);
-      } else if ((tid >> 5) == kReducerWarp) {
+      }
+      if ((tid >> 5) == kReducerWarp) {
+        // slots first (then arrive at the pass-end barrier), owned level-1
+        // nodes after -- overlapping the grid barrier
         tma_reduce<C, true>(a, rs, sp, &a.ctl->tile_next[1], l1, it);
         if ((tid & 31) == 0) probe(a, it, 7, global_ns());
+      } else {
+        bar_sync_end();
       }
-    } else if (it == 0) {
-      tma_consume_seed<XT, C, MODE>(a, smem, ps, rs, sp, pw);
     } else {
-      double v[C];
+      if (it == 0) {
+        tma_consume_seed<XT, C, MODE>(a, smem, ps, rs, sp, pw);
+      } else {
+        double v[C];
 #pragma unroll
-      for (int j = 0; j < C; ++j) v[j] = j < c ? vsh[j] : 0.0;
-      double lwx[C], lwb[C], ljb = 0.0;
-      if (LUT) tma_build_lut<C>(smem + L::kLutOff, v, c, pw, lwx, lwb, ljb);
-      if (MODE == MODE_LUT2) tma_build_lut2<C>(smem + L::kLutOff, v);
-      tma_consume<XT, C, MODE>(a, smem, ps, rs, sp, v, pw, lwx, lwb, ljb);
-      if (tid == 0) probe(a, it, 2, global_ns());
+        for (int j = 0; j < C; ++j) v[j] = j < c ? vsh[j] : 0.0;
+        double lwx[C], lwb[C], ljb = 0.0;
+        if (LUT) tma_build_lut<C>(smem + L::kLutOff, v, c, pw, lwx, lwb, ljb);
+        if (MODE == MODE_LUT2) tma_build_lut2<C>(smem + L::kLutOff, v);
+        tma_consume<XT, C, MODE>(a, smem, ps, rs, sp, v, pw, lwx, lwb, ljb);
+        if (tid == 0) probe(a, it, 2, global_ns());
+      }
+      bar_sync_end();
     }
-    __syncthreads();
-    ++gen;  // every thread: gen selects the level-1 half below
+    gen = gnext;
     if (tid == 0) {
-      if (!grid_barrier(a.ctl, gen, gridDim.x)) s_done = 1;
+      if (!grid_barrier(a.ctl, gen, gridDim.x) || !wait_count(&a.ctl->l1_done, gen * l1_real)) {
+        a.ctl->dead = -3;  // a stuck CTA (cannot happen with co-resident CTAs): flag the run
+        a.ctl->done = 1;
+        s_done = 1;
+      }
       probe(a, it, 3, global_ns());
     }
     __syncthreads();
