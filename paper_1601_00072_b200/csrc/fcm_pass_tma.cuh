@@ -1314,7 +1314,11 @@ inline cudaError_t launch_loop_tma(const PassArgs& a, int sms, cudaStream_t st, 
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kTmaThreads, L::kSmemBytes);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorCooperativeLaunchTooLarge;
-  long long g = (long long)per_sm * sms / (share > 0 ? share : 1);
+  // kernels sharing a device (multi-shard plans on one GPU) each take at most
+  // half their fair share of CTA slots: concurrent cooperative launches are
+  // not co-scheduled by contract, so leave slack for imperfect packing
+  long long g = (long long)per_sm * sms;
+  if (share > 1) g = std::max(1LL, g / (2LL * share));
   if (force_grid > 0 && force_grid < g) g = force_grid;
   if (g > a.g.tiles_local) g = a.g.tiles_local;
   if (g < 1) g = 1;
