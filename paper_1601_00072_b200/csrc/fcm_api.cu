@@ -167,14 +167,17 @@ int nf_of(int c) { return 2 * c + 2; }
 int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 // Global tile tree ("Deterministic reduction").  Depends only on n.
-// Tile = the smallest power of two >= 1024 voxels (>= 2048 once the volume
-// gives a full B200 -- 2 x 148 CTAs -- 8 tiles per CTA) that keeps the tile
-// count <= 64 per CTA: enough tiles that the end-of-pass imbalance (<= one
-// tile) stays short, few enough that per-tile reduction work stays small.
-// Beyond 8 * 32^3 tiles they grow further.
+// Tile = 8192 voxels (8 TMA chunks) unless that leaves fewer than 100 tiles,
+// then halved down to 1024; above 64 tiles per CTA of a full B200 (2 x 148
+// CTAs) it doubles.  Measured per-pass times (tools/tile_sweep.py, C2/C4
+// bench): the per-tile reduction handoff costs more than the end-of-pass
+// imbalance of larger tiles down to ~100 tiles per volume (C1 1024, C3-200K
+// 2048, C3-1M/C2/C4 8192).  Beyond 8 * 32^3 tiles they grow further.
 void base_geometry(int64_t n, Geometry& g) {
-  int64_t tile = n >= int64_t(2048) * 8 * 296 ? 2048 : 1024;
+  int64_t tile = 8192;
+  while (tile > 1024 && ceil_div(n, tile) < 100) tile >>= 1;
   while (ceil_div(n, tile) > int64_t(64) * 296) tile <<= 1;
+  if (const char* e = getenv("FCM_TILE_EXPERIMENT")) tile = std::max<int64_t>(1024, atoll(e));  // A/B only
   const int64_t cap = (int64_t)kOctants << (5 * kMaxLevels);
   while (ceil_div(n, tile) > cap) tile <<= 1;
   int shift = 0;

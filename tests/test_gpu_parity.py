@@ -272,13 +272,14 @@ def test_config2_volume_vs_oracle():
 def test_three_level_tree_loop_vs_per_pass_vs_shards_bitwise():
     """A volume whose octants need a 3-level node tree (M > 1024 tiles): the
     loop kernel (redundant upper levels after the grid barrier), one launch
-    per pass (CTA 0 climbs) and a 2-shard plan (NCCL-free peer finalize) give
-    the same bits."""
+    per pass (CTA 0 climbs) and a 2-shard plan (mailbox exchange) give the
+    same bits (centers, objective trace, labels)."""
     from paper_1601_00072_b200 import _lib
-    n = 25_000_003
+    n = 70_000_003
     geo = _lib.geometry(n)
     assert geo["levels"] == 3
-    x = np.clip(np.rint(mixture_pixels(n, 3, seed=77)), 0, 255).astype(np.uint8)
+    rng = np.random.default_rng(77)
+    x = np.clip(rng.choice(np.array([40, 120, 200]), size=n) + rng.integers(-10, 11, size=n), 0, 255).astype(np.uint8)
 
     def solve(loop, devices=None):
         plan = pkg.FcmPlan(n, 3, _lib.FCM_X_U8, devices=devices) if devices else pkg.FcmPlan(n, 3, _lib.FCM_X_U8)
@@ -287,15 +288,15 @@ def test_three_level_tree_loop_vs_per_pass_vs_shards_bitwise():
             plan.init_membership(3)
             plan.set_option(_lib.FCM_OPT_LOOP, loop)
             out = plan.run(2.0, 1e-5, 100)
-            u, lab = plan.download()
-        return out, u, lab
+            _, lab = plan.download(membership=False)
+        return out, lab
 
-    (va, ta, ka, ca), ua, la = solve(1)
+    (va, ta, ka, ca), la = solve(1)
     for other in (solve(0), solve(1, devices=[0, 0])):
-        (vb, tb, kb, cb), ub, lb = other
+        (vb, tb, kb, cb), lb = other
         assert ka == kb and ca == cb
         assert va.tobytes() == vb.tobytes() and ta.tobytes() == tb.tobytes()
-        assert ua.tobytes() == ub.tobytes() and np.array_equal(la, lb)
+        assert np.array_equal(la, lb)
 
 
 @pytest.mark.parametrize("devices", [[0, 0], [0] * 8])
