@@ -25,6 +25,7 @@ constexpr int kTmaThreads = kThreads + 64;  // consumers | producer warp | reduc
 constexpr int kProducerTid = kThreads;
 constexpr int kReducerWarp = kThreads / 32 + 1;
 constexpr int kSlots = 8;  // tile-partial slots between consumers and the reducer (<= 32)
+constexpr int kSmallTiles = 1024;  // loop kernel: up to this many tiles every CTA reduces level 1 itself
 
 // Consumer -> reducer handoff: per slot, the 8 warp-tree values of every
 // field of one tile (tile = -1: end of pass).  full: 8 warp arrivals;
@@ -556,7 +557,7 @@ template <typename XT, int C, int MODE>
 __device__ __forceinline__ void tma_consume(const PassArgs& a, uint8_t* smem, Pipe& ps,
                                             RedSlots<2 * C + 2>& rs, Pipe& sp, const double* v,
                                             const Powers& pw, const double* lwx = nullptr,
-                                            const double* lwb = nullptr, double ljb = 0.0) {
+                                            const double* lwb = nullptr, double ljb = 0.0, unsigned it = 0) {
   constexpr bool LUT = MODE == MODE_LUT;
   constexpr bool LUT2 = MODE == MODE_LUT2;
   using L = TmaLayout<XT, C, MODE>;
@@ -577,8 +578,12 @@ __device__ __forceinline__ void tma_consume(const PassArgs& a, uint8_t* smem, Pi
   uint32_t dmax_hi = 0;
   uint32_t* hist = reinterpret_cast<uint32_t*>(smem + L::kLutOff + (LUT ? LL::kHistOff : 0));
   int hpar = 0;  // histogram buffer of the current tile
+  bool first = true;
+  if (it && tid == 0) probe(a, it, 13, global_ns());
   for (;;) {
     mbar_wait(bar0 + 8u * ps.stage, ps.phase);
+    if (first && it && tid == 0) probe(a, it, 12, global_ns());
+    first = false;
     const StageMeta mt = meta[ps.stage];
     const uint8_t* st = smem + ps.stage * L::kStageBytes;
     if (mt.tile < 0) {
@@ -776,14 +781,15 @@ __device__ __forceinline__ void upper_node(const Geometry& g, int k, int& l, int
 //     (octant by octant), the rank root and the finalize.
 template <int C, bool LOOP>
 __device__ __forceinline__ void tma_reduce(const PassArgs& a, RedSlots<2 * C + 2>& rs, Pipe& sp,
-                                           const unsigned* counter, double* l1_out, unsigned it = 0) {
+                                           const unsigned* counter, double* l1_out, unsigned it = 0,
+                                           bool no_owners = false) {
   constexpr int NF = 2 * C + 2;
   const int lane = threadIdx.x & 31;
   const int nf = 2 * a.c + 2;
   const Geometry& g = a.g;
   const int G = gridDim.x;
   const bool cta0 = blockIdx.x == 0;
-  const int NA = g.noct * g.nodes[1];  // list A: level-1 nodes
+  const int NA = no_owners ? 0 : g.noct * g.nodes[1];  // list A: level-1 nodes
   int per = 0;
   for (int m = 2; m <= g.levels; ++m) per += g.nodes[m];
   const int NB = (!LOOP && cta0) ? g.noct * per : 0;  // list B: CTA 0's upper levels
@@ -800,11 +806,15 @@ __device__ __forceinline__ void tma_reduce(const PassArgs& a, RedSlots<2 * C + 2
   uint64_t n_poll = 0, n_node = 0;
 
   uint32_t backoff = 64;
+  bool node_hot = false;  // the pending node's tiles have all been handed out
   while (!slots_done || za < NA || zb < NB) {
     // next slot: sleep in hardware until it fills (bounded while a node is
     // pending, so the node is still polled about every microsecond)
-    if (!slots_done && ((za < NA || zb < NB) ? mbar_wait_for(smem_u32(&rs.full[sp.stage]), sp.phase, 1000)
-                                             : (mbar_wait(smem_u32(&rs.full[sp.stage]), sp.phase), true))) {
+    // (a node whose tiles are all handed out is "hot": poll it every ~200 ns)
+    const bool pending = za < NA || zb < NB;
+    const uint32_t hint = pending && node_hot ? 200u : 1000u;
+    if (!slots_done && (pending ? mbar_wait_for(smem_u32(&rs.full[sp.stage]), sp.phase, hint)
+                                : (mbar_wait(smem_u32(&rs.full[sp.stage]), sp.phase), true))) {
       const int t = rs.tile[sp.stage];
       if (t >= 0) {
         for (int f = lane; f < nf; f += 32) {  // nf <= 34
@@ -822,7 +832,10 @@ __device__ __forceinline__ void tma_reduce(const PassArgs& a, RedSlots<2 * C + 2
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(&rs.empty[sp.stage]));
       sp.advance<kSlots>();
-      if (LOOP && slots_done) bar_arrive_end();  // the CTA may enter the grid barrier now
+      if (LOOP && slots_done) {
+        bar_arrive_end();  // the CTA may enter the grid barrier now
+        if (it && lane == 0) probe(a, it, 15, global_ns());
+      }
       continue;
     }
     int l, lo, j;
@@ -845,7 +858,8 @@ __device__ __forceinline__ void tma_reduce(const PassArgs& a, RedSlots<2 * C + 2
       const int last_lt = (int)((long long)oct * g.M - g.tile0 + last);
       // (loop kernel, after this CTA's slots: the barrier may already have
       // re-armed the scheduler, so poll without the hand-out check)
-      if ((LOOP && slots_done) || (int)ld_relaxed_u32(counter) > last_lt) {
+      node_hot = (LOOP && slots_done) || (int)ld_relaxed_u32(counter) > last_lt;
+      if (node_hot) {
         ++n_poll;
         double* child0 = l == 1 ? a.tile_part + ((int64_t)oct * g.M - g.tile0 + (int64_t)j * kFan) * nf
                                 : a.node_part[l - 1] + ((int64_t)lo * g.nodes[l - 1] + (int64_t)j * kFan) * nf;
@@ -865,6 +879,7 @@ __device__ __forceinline__ void tma_reduce(const PassArgs& a, RedSlots<2 * C + 2
       if (za < NA) za += strideA;
       else ++zb;
       backoff = 64;
+      node_hot = false;
     } else if (slots_done) {
       __nanosleep(backoff);  // pass drained: poll the pending node with a short backoff
       backoff = min(backoff * 2, 128u);
@@ -913,11 +928,29 @@ __device__ __forceinline__ double tree32(const double* p, int64_t stride, int nr
 // tree32; all kTmaThreads threads call it; scratch is the (idle) stage ring.
 template <int NF>
 __device__ __forceinline__ void loop_upper(const PassArgs& a, const double* l1, double* scratch,
-                                           double (*oroot)[NF], double* root, unsigned it = 0) {
+                                           double (*oroot)[NF], double* root, unsigned it = 0,
+                                           bool from_tiles = false) {
   const int tid = threadIdx.x;
   const int nf = 2 * a.c + 2;
   const Geometry& g = a.g;
   const int per = g.levels == 3 ? g.nodes[2] : 1;
+  // step 0 (small volumes, no level-1 owners): the level-1 nodes themselves,
+  // from the tile partials the grid barrier published, into shared memory
+  if (from_tiles) {
+    double* l1s = scratch;
+    scratch += (int64_t)g.noct * g.nodes[1] * NF;
+    for (int pr = tid; pr < g.noct * g.nodes[1] * nf; pr += kTmaThreads) {
+      const int z = pr / nf, f = pr - z * nf;
+      const int lo = z / g.nodes[1], j = z - lo * g.nodes[1];
+      const int oct = g.oct0 + lo;
+      const int nreal = (int64_t)oct * g.M < g.T ? node_real_children(g, oct, 1, j) : 0;
+      const double* src = a.tile_part + ((int64_t)oct * g.M - g.tile0 + (int64_t)j * kFan) * nf + f;
+      l1s[(int64_t)z * NF + f] = nreal ? tree32<true>(src, nf, nreal, f == nf - 1) : 0.0;
+    }
+    __syncthreads();
+    l1 = l1s;
+  }
+  const int ls = from_tiles ? NF : nf;  // row stride of the level-1 results
   // step 1: level-2 nodes (L == 3) or octant roots (L == 2) from level-1 results
   if (g.levels >= 2) {
     for (int pr = tid; pr < g.noct * per * nf; pr += kTmaThreads) {
@@ -925,8 +958,10 @@ __device__ __forceinline__ void loop_upper(const PassArgs& a, const double* l1, 
       const int lo = item / per, k = item - lo * per;
       const int oct = g.oct0 + lo;
       const int nreal = (int64_t)oct * g.M < g.T ? node_real_children(g, oct, 2, k) : 0;
-      const double* src = l1 + ((int64_t)lo * g.nodes[1] + (int64_t)k * kFan) * nf + f;
-      scratch[(int64_t)item * NF + f] = nreal ? tree32<true>(src, nf, nreal, f == nf - 1) : 0.0;
+      const double* src = l1 + ((int64_t)lo * g.nodes[1] + (int64_t)k * kFan) * ls + f;
+      double r = 0.0;
+      if (nreal) r = from_tiles ? tree32<false>(src, ls, nreal, f == nf - 1) : tree32<true>(src, ls, nreal, f == nf - 1);
+      scratch[(int64_t)item * NF + f] = r;
     }
     __syncthreads();
     if (tid == 0) probe(a, it, 11, global_ns());
@@ -937,7 +972,8 @@ __device__ __forceinline__ void loop_upper(const PassArgs& a, const double* l1, 
     const int oct = g.oct0 + lo;
     double r = 0.0;
     if ((int64_t)oct * g.M < g.T) {
-      if (g.levels == 1) r = __ldcg(l1 + (int64_t)lo * nf + f);  // the level-1 node is the octant root
+      if (g.levels == 1)  // the level-1 node is the octant root
+        r = from_tiles ? l1[(int64_t)lo * ls + f] : __ldcg(l1 + (int64_t)lo * ls + f);
       else if (g.levels == 2) r = scratch[(int64_t)lo * NF + f];
       else r = tree32<false>(scratch + (int64_t)lo * per * NF + f, NF, (int)octant_real_nodes(g, oct, 2), f == nf - 1);
     }
@@ -1186,7 +1222,8 @@ __global__ void __launch_bounds__(kTmaThreads, 2) loop_tma_kernel(PassArgs a) {
   constexpr bool LUT = MODE == MODE_LUT;
   constexpr int NF = 2 * C + 2;
   using L = TmaLayout<XT, C, MODE>;
-  static_assert(L::kRingBytes >= kOctants * kFan * NF * 8, "ring too small for the upper-level scratch");
+  static_assert(L::kRingBytes >= (kOctants * kFan + kSmallTiles / kFan + kOctants) * NF * 8,
+                "ring too small for the upper-level scratch");
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ RedSlots<NF> rs;
   __shared__ double oroot[kOctants][NF];
@@ -1202,8 +1239,12 @@ __global__ void __launch_bounds__(kTmaThreads, 2) loop_tma_kernel(PassArgs a) {
   }
   const Powers pw = load_powers(a);
   const int64_t l1_len = (int64_t)a.g.noct * a.g.nodes[1] * (2 * a.c + 2);  // one of 3 buffers
+  // small volumes (<= 1024 tiles): no level-1 owners -- every CTA reduces
+  // the level-1 nodes itself after the grid barrier (one hop less per pass)
+  const bool from_tiles = a.g.tiles_local <= kSmallTiles;
   unsigned l1_real = 0;  // real level-1 nodes of this rank (published once per pass)
-  for (int lo = 0; lo < a.g.noct; ++lo) l1_real += (unsigned)octant_real_nodes(a.g, a.g.oct0 + lo, 1);
+  if (!from_tiles)
+    for (int lo = 0; lo < a.g.noct; ++lo) l1_real += (unsigned)octant_real_nodes(a.g, a.g.oct0 + lo, 1);
   Pipe ps, sp;
   unsigned gen = 0;  // grid-barrier generations
   __syncthreads();
@@ -1227,7 +1268,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) loop_tma_kernel(PassArgs a) {
       if ((tid >> 5) == kReducerWarp) {
         // slots first (then arrive at the pass-end barrier), owned level-1
         // nodes after -- overlapping the grid barrier
-        tma_reduce<C, true>(a, rs, sp, &a.ctl->tile_next[1], l1, it);
+        tma_reduce<C, true>(a, rs, sp, &a.ctl->tile_next[1], l1, it, from_tiles);
         if ((tid & 31) == 0) probe(a, it, 7, global_ns());
       } else {
         bar_sync_end();
@@ -1242,7 +1283,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) loop_tma_kernel(PassArgs a) {
         double lwx[C], lwb[C], ljb = 0.0;
         if (LUT) tma_build_lut<C>(smem + L::kLutOff, v, c, pw, lwx, lwb, ljb);
         if (MODE == MODE_LUT2) tma_build_lut2<C>(smem + L::kLutOff, v);
-        tma_consume<XT, C, MODE>(a, smem, ps, rs, sp, v, pw, lwx, lwb, ljb);
+        tma_consume<XT, C, MODE>(a, smem, ps, rs, sp, v, pw, lwx, lwb, ljb, it);
         if (tid == 0) probe(a, it, 2, global_ns());
       }
       bar_sync_end();
@@ -1258,7 +1299,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) loop_tma_kernel(PassArgs a) {
     }
     __syncthreads();
     if (s_done) break;
-    loop_upper<NF>(a, l1, reinterpret_cast<double*>(smem), oroot, rs.root, it);
+    loop_upper<NF>(a, l1, reinterpret_cast<double*>(smem), oroot, rs.root, it, from_tiles);
     if (tid == 0) probe(a, it, 10, global_ns());
     if (a.mb_ranks > 1 && !exchange_roots(a, rs.root, gen)) {
       if (tid == 0) {

@@ -64,3 +64,14 @@ def mx(j, it=1):
     return (int(P[it, :, j].max()) - int(P[it, :, 0].min())) / 1e3
 print("pass 2 chain (max over CTAs, us from pass start): consumers", mx(2), "reducers", mx(7), "barrier", mx(3),
       "upper step1", mx(11), "upper done", mx(10), "finalize", mx(14), "next start", (int(P[2, :, 0].max()) - int(P[1, :, 0].min())) / 1e3)
+
+def mn(j, it=1):
+    return (np.median(P[it, :, j].astype(np.int64)) - int(P[it, :, 0].min())) / 1e3
+print("pass 2 start (median over CTAs, us): consumers start", mn(13), "first stage", mn(12), "| max:", mx(13), mx(12))
+
+b0 = int(P[1, :, 0].min())
+red = P[1, :, 7].astype(np.int64) - b0
+o = np.argsort(red)[-5:]
+print("slowest reducers (cta, slots done, reducer done, consumers done, nodes, polls):")
+for b in o:
+    print(int(b), (int(P[1, b, 15]) - b0) / 1e3, red[b] / 1e3, (int(P[1, b, 2]) - b0) / 1e3, int(P[1, b, 9]), int(P[1, b, 8]))
