@@ -96,3 +96,13 @@ def test_gloo_two_rank_exchange_matches_single(tmp_path):
     got = np.load(out)
     ref = rank_root(_partials(geometry(n, 1, 0)["T"], 8, seed=5), geometry(n, 1, 0))
     assert got.tobytes() == ref.tobytes()
+
+
+@pytest.mark.parametrize("n,tile", [(39277, 1024), (78554, 1024), (235662, 2048), (628432, 4096),
+                                    (1178310, 8192), (7109137, 8192), (134217728, 8192), (536870912, 32768)])
+def test_tile_size_rule(n, tile):
+    """Tile sizes chosen by base_geometry (DESIGN 3.4; measured with tools/tile_sweep.py):
+    8192 voxels, halved while fewer than 100 tiles remain (>= 1024), doubled above 64 tiles per CTA."""
+    g = geometry(n)
+    assert g["tile"] == tile
+    assert g["T"] <= 64 * 296 or tile == 1024
