@@ -1,0 +1,243 @@
+// fcm_tma_kernels.cuh -- the TMA kernels: one pass per launch
+// (pass_tma_kernel) and the persistent loop kernel, plus their launchers.
+// Part of fcm_pass_tma.cuh.
+#pragma once
+#include "fcm_tma_tree.cuh"
+
+namespace fcm {
+
+template <typename XT, int C, int MODE>
+__device__ __forceinline__ void tma_init_barriers(uint8_t* smem, RedSlots<2 * C + 2>& rs) {
+  using L = TmaLayout<XT, C, MODE>;
+  const uint32_t bar0 = smem_u32(smem + L::kBarOff);
+  for (int s = 0; s < L::kStages; ++s) {
+    mbar_init(bar0 + 8u * s, 1);
+    mbar_init(bar0 + 8u * (L::kStages + s), kWarps);
+  }
+  for (int s = 0; s < kSlots; ++s) {
+    mbar_init(smem_u32(&rs.full[s]), kWarps);
+    mbar_init(smem_u32(&rs.empty[s]), 1);
+  }
+  mbar_fence_init();
+}
+
+template <int C>
+__device__ __forceinline__ void load_centers(const Control* ctl, int c, double* v) {
+#pragma unroll
+  for (int j = 0; j < C; ++j) v[j] = j < c ? __ldcg(&ctl->v[j]) : 0.0;
+}
+
+// ------------------------------------------------- one pass per launch ----
+template <typename XT, int C, int MODE>
+__global__ void __launch_bounds__(kTmaThreads, 2) pass_tma_kernel(PassArgs a) {
+  constexpr bool LUT = MODE == MODE_LUT;
+  using L = TmaLayout<XT, C, MODE>;
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ RedSlots<2 * C + 2> rs;
+  __shared__ int s_done;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    int done = *(volatile int*)&a.ctl->done;
+    if (blockIdx.x == 0 && a.seq != 0) {
+      const unsigned launched = a.ctl->launches++;
+      if (!done && a.use_cond && launched > (unsigned)a.max_iters + 8u) {
+        a.ctl->dead = -2;  // watchdog: a device loop may never outlive max_iters passes
+        a.ctl->done = 1;
+        done = 1;
+      }
+      if (done && a.use_cond) cudaGraphSetConditional(a.cond, 0u);
+    }
+    s_done = done;
+    if (!done) {
+      tma_init_barriers<XT, C, MODE>(smem, rs);
+      if (blockIdx.x == 0) a.ctl->tile_next[(a.seq + 1) & 1] = 0u;
+    }
+  }
+  __syncthreads();
+  if (s_done) return;
+  Pipe ps, sp;
+  if (tid >= kThreads) {
+    if (tid == kProducerTid) tma_produce<XT, C, MODE>(a, smem, ps, &a.ctl->tile_next[a.seq & 1]);
+    else if ((tid >> 5) == kReducerWarp)
+      tma_reduce<C, false>(a, rs, sp, &a.ctl->tile_next[a.seq & 1], nullptr);
+    return;
+  }
+  const int c = C <= 8 ? C : a.c;
+  double v[C];
+  load_centers<C>(a.ctl, c, v);
+  const Powers pw = load_powers(a);
+  double lwx[C], lwb[C], ljb = 0.0;
+  if (LUT) tma_build_lut<C>(smem + L::kLutOff, v, c, pw, lwx, lwb, ljb);
+  if (MODE == MODE_LUT2) tma_build_lut2<C>(smem + L::kLutOff, v);
+  tma_consume<XT, C, MODE>(a, smem, ps, rs, sp, v, pw, lwx, lwb, ljb);
+}
+
+// --------------------------------------------- persistent loop kernel -----
+// The whole device loop of core._iterate (core.py:118-131) in ONE launch:
+// every CTA stays resident (cooperative launch), runs pass after pass over
+// the dynamic tile scheduler, and meets the others at a grid barrier between
+// passes; the CTA that completes a pass's reduction tree finalizes v_{k+1}
+// and the stop test before it arrives.  u is updated in place.  No
+// per-iteration launch, no host round trip, ring barriers initialised once.
+template <typename XT, int C, int MODE>
+__global__ void __launch_bounds__(kTmaThreads, 2) loop_tma_kernel(PassArgs a) {
+  constexpr bool LUT = MODE == MODE_LUT;
+  constexpr int NF = 2 * C + 2;
+  using L = TmaLayout<XT, C, MODE>;
+  static_assert(L::kRingBytes >= (kOctants * kFan + kSmallTiles / kFan + kOctants) * NF * 8,
+                "ring too small for the upper-level scratch");
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ RedSlots<NF> rs;
+  __shared__ double oroot[kOctants][NF];
+  __shared__ double vsh[C];
+  __shared__ double vnew[C];
+  __shared__ int s_done;
+  const int tid = threadIdx.x;
+  const int c = C <= 8 ? C : a.c;
+  if (tid == 0) {
+    tma_init_barriers<XT, C, MODE>(smem, rs);
+    s_done = *(volatile int*)&a.ctl->done;
+    for (int j = 0; j < c; ++j) vsh[j] = __ldcg(&a.ctl->v[j]);
+  }
+  const Powers pw = load_powers(a);
+  const int64_t l1_len = (int64_t)a.g.noct * a.g.nodes[1] * (2 * a.c + 2);  // one of 3 buffers
+  // small volumes (<= 1024 tiles): no level-1 owners -- every CTA reduces
+  // the level-1 nodes itself after the grid barrier (one hop less per pass)
+  const bool from_tiles = a.g.tiles_local <= kSmallTiles;
+  unsigned l1_real = 0;  // real level-1 nodes of this rank (published once per pass)
+  if (!from_tiles)
+    for (int lo = 0; lo < a.g.noct; ++lo) l1_real += (unsigned)octant_real_nodes(a.g, a.g.oct0 + lo, 1);
+  Pipe ps, sp;
+  unsigned gen = 0;  // grid-barrier generations
+  __syncthreads();
+  for (unsigned it = a.seed_pass ? 0u : 1u; !s_done && it <= (unsigned)a.max_iters; ++it) {
+    if (tid == 0) probe(a, it, 0, global_ns());
+    // level-1 results of this pass: buffer (gen+1) % 3; owners publish them
+    // after their CTA has entered the grid barrier and count them in
+    // ctl->l1_done (fence + atomic per node); readers wait for the count
+    const unsigned gnext = gen + 1;
+    double* l1 = a.l1_buf + (gnext % 3) * l1_len;
+    if (tid >= kThreads) {
+      if (tid == kProducerTid) {
+        fence_proxy_async_global();
+        const int n = tma_produce<XT, C, MODE>(a, smem, ps, &a.ctl->tile_next[1], it, it == 0);
+        probe(a, it, 1, global_ns());
+        probe(a, it, 4, (uint64_t)n);
+        unsigned smid;
+        asm("mov.u32 %0, %%smid;" : "=r"(smid));
+        probe(a, it, 6, smid);
+      }
+      if ((tid >> 5) == kReducerWarp) {
+        // slots first (then arrive at the pass-end barrier), owned level-1
+        // nodes after -- overlapping the grid barrier
+        tma_reduce<C, true>(a, rs, sp, &a.ctl->tile_next[1], l1, it, from_tiles);
+        if ((tid & 31) == 0) probe(a, it, 7, global_ns());
+      } else {
+        bar_sync_end();
+      }
+    } else {
+      if (it == 0) {
+        tma_consume_seed<XT, C, MODE>(a, smem, ps, rs, sp, pw);
+      } else {
+        double v[C];
+#pragma unroll
+        for (int j = 0; j < C; ++j) v[j] = j < c ? vsh[j] : 0.0;
+        double lwx[C], lwb[C], ljb = 0.0;
+        if (LUT) tma_build_lut<C>(smem + L::kLutOff, v, c, pw, lwx, lwb, ljb);
+        if (MODE == MODE_LUT2) tma_build_lut2<C>(smem + L::kLutOff, v);
+        tma_consume<XT, C, MODE>(a, smem, ps, rs, sp, v, pw, lwx, lwb, ljb, it);
+        if (tid == 0) probe(a, it, 2, global_ns());
+      }
+      bar_sync_end();
+    }
+    gen = gnext;
+    if (tid == 0) {
+      if (!grid_barrier(a.ctl, gen, gridDim.x) || !wait_count(&a.ctl->l1_done, gen * l1_real)) {
+        a.ctl->dead = -3;  // a stuck CTA (cannot happen with co-resident CTAs): flag the run
+        a.ctl->done = 1;
+        s_done = 1;
+      }
+      probe(a, it, 3, global_ns());
+    }
+    __syncthreads();
+    if (s_done) break;
+    loop_upper<NF>(a, l1, reinterpret_cast<double*>(smem), oroot, rs.root, it, from_tiles);
+    if (tid == 0) probe(a, it, 10, global_ns());
+    if (a.mb_ranks > 1 && !exchange_roots(a, rs.root, gen)) {
+      if (tid == 0) {
+        a.ctl->dead = -3;
+        a.ctl->done = 1;
+      }
+      break;
+    }
+    if (tid < c) vnew[tid] = rs.root[tid] / rs.root[c + tid];  // the c divisions side by side
+    __syncthreads();
+    if (tid == 0) {
+      finalize_loop(a, rs.root, it, vsh, vnew, &s_done);
+      probe(a, it, 14, global_ns());
+    }
+    __syncthreads();
+  }
+}
+
+template <typename XT, int C, int MODE>
+inline cudaError_t launch_pass_tma(const PassArgs& a, int sms, cudaStream_t st, int* grid_out,
+                                   int force_grid) {
+  using L = TmaLayout<XT, C, MODE>;
+  auto k = pass_tma_kernel<XT, C, MODE>;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  static unsigned configured = 0;  // per instantiation, bit per device
+  if (dev >= 32 || !(configured & (1u << dev))) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kSmemBytes);
+    if (e != cudaSuccess) return e;
+    if (dev < 32) configured |= 1u << dev;
+  }
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kTmaThreads, L::kSmemBytes);
+  if (per_sm < 1) per_sm = 1;
+  long long g = force_grid > 0 ? force_grid : (long long)per_sm * sms;
+  if (g > a.g.tiles_local) g = a.g.tiles_local;
+  if (g < 1) g = 1;
+  k<<<(int)g, kTmaThreads, L::kSmemBytes, st>>>(a);
+  if (grid_out) *grid_out = (int)g;
+  return cudaGetLastError();
+}
+
+// The persistent loop kernel needs every CTA resident at once: cooperative
+// launch (fails instead of deadlocking when the grid cannot be co-resident).
+template <typename XT, int C, int MODE>
+inline cudaError_t launch_loop_tma(const PassArgs& a, int sms, cudaStream_t st, int* grid_out,
+                                   int force_grid, int share = 1) {
+  using L = TmaLayout<XT, C, MODE>;
+  auto k = loop_tma_kernel<XT, C, MODE>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kSmemBytes);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kTmaThreads, L::kSmemBytes);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorCooperativeLaunchTooLarge;
+  // kernels sharing a device (multi-shard plans on one GPU) each take at most
+  // half their fair share of CTA slots: concurrent cooperative launches are
+  // not co-scheduled by contract, so leave slack for imperfect packing
+  long long g = (long long)per_sm * sms;
+  if (share > 1) g = std::max(1LL, g / (2LL * share));
+  if (force_grid > 0 && force_grid < g) g = force_grid;
+  if (g > a.g.tiles_local) g = a.g.tiles_local;
+  if (g < 1) g = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)g);
+  cfg.blockDim = dim3(kTmaThreads);
+  cfg.dynamicSmemBytes = L::kSmemBytes;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, k, a);
+  if (grid_out) *grid_out = (int)g;
+  return e;
+}
+
+}  // namespace fcm

@@ -1,0 +1,440 @@
+// fcm_tma_tree.cuh -- the reduction half of the TMA pass: reducer warp,
+// fence-free publication of tile partials, level-1 owners, the upper tree
+// levels, the grid barrier, the loop kernel's stop test and the multi-rank
+// mailbox exchange.  Part of fcm_pass_tma.cuh.
+#pragma once
+#include "fcm_tma_pipe.cuh"
+
+namespace fcm {
+
+// ------------------------------------------------------------- reducer ----
+// Poll-and-reduce of one tree node by one warp: lane i reads child i's NF
+// fields (children < nreal; the rest count as 0.0).  Returns false, without
+// side effects, while any child is unpublished; otherwise resets the children
+// to unpublished and leaves the per-field adjacent-pair warp tree in lane 0
+// of out[f] (out in shared or global memory, written by lane 0).
+template <int NF, bool GLOBAL_OUT>
+__device__ __forceinline__ bool try_node(double* child0, int nreal, int nf, double* out) {
+  const int lane = threadIdx.x & 31;
+  const bool real = lane < nreal;
+  double* src = child0 + (int64_t)lane * nf;
+  // one round trip: every field of every child in flight at once, then check
+  double v[NF];
+#pragma unroll
+  for (int f = 0; f < NF; ++f) v[f] = (f < nf && real) ? ld_relaxed(src + f) : 0.0;
+  bool ok = true;
+#pragma unroll
+  for (int f = 0; f < NF; ++f)
+    if (f < nf && real) ok = ok && !is_sentinel(v[f]);
+  if (!__all_sync(0xffffffffu, ok)) return false;
+#pragma unroll
+  for (int f = 0; f < NF; ++f)
+    if (f < nf) {
+      if (real) st_relaxed(src + f, sentinel());
+      const double r = warp_tree(v[f], f == nf - 1);
+      if (lane == 0) {
+        if (GLOBAL_OUT) st_relaxed(out + f, r);
+        else out[f] = r;
+      }
+    }
+  return true;
+}
+
+template <int NF, bool GLOBAL_OUT>
+__device__ __forceinline__ void wait_node(double* child0, int nreal, int nf, double* out) {
+  while (!try_node<NF, GLOBAL_OUT>(child0, nreal, nf, out)) __nanosleep(32);
+}
+
+// Node k of CTA 0's upper-level list -- levels 2..L, octant by octant, each
+// octant's level-2 nodes before its level-3 node -- as (level, octant, j).
+__device__ __forceinline__ void upper_node(const Geometry& g, int k, int& l, int& lo, int& j) {
+  int per = 0;
+  for (int m = 2; m <= g.levels; ++m) per += g.nodes[m];
+  lo = k / per;
+  j = k - lo * per;
+  l = 2;
+  while (j >= g.nodes[l]) {
+    j -= g.nodes[l];
+    ++l;
+  }
+}
+
+// One warp per CTA.  It (1) drains the consumers' slots: per slot the 8-warp
+// pair tree per field (the top three levels of the tile's binary tree over
+// its 256 threads) and a relaxed publish of the tile partial -- no fence, no
+// atomic on the streaming path; (2) in the gaps, reduces the level-1 nodes
+// this CTA owns once the scheduler has handed out all their tiles and every
+// child is visibly published (fixed owners: no last-arriver races, no
+// feedback onto slow CTAs).
+//   LOOP (persistent kernel): level-1 node z belongs to CTA z mod G and its
+//     result goes to l1_out (plain stores; the grid barrier that follows
+//     publishes it, every CTA then reduces the levels above redundantly);
+//   per-pass kernels: node z belongs to CTA 1 + z mod (G-1), results are
+//     published with the sentinel protocol, and CTA 0 owns the levels above
+//     (octant by octant), the rank root and the finalize.
+template <int C, bool LOOP>
+__device__ __forceinline__ void tma_reduce(const PassArgs& a, RedSlots<2 * C + 2>& rs, Pipe& sp,
+                                           const unsigned* counter, double* l1_out, unsigned it = 0,
+                                           bool no_owners = false) {
+  constexpr int NF = 2 * C + 2;
+  const int lane = threadIdx.x & 31;
+  const int nf = 2 * a.c + 2;
+  const Geometry& g = a.g;
+  const int G = gridDim.x;
+  const bool cta0 = blockIdx.x == 0;
+  const int NA = no_owners ? 0 : g.noct * g.nodes[1];  // list A: level-1 nodes
+  int per = 0;
+  for (int m = 2; m <= g.levels; ++m) per += g.nodes[m];
+  const int NB = (!LOOP && cta0) ? g.noct * per : 0;  // list B: CTA 0's upper levels
+  int strideA, za;
+  if (LOOP || G == 1) {
+    strideA = G;
+    za = blockIdx.x;
+  } else {
+    strideA = G - 1;
+    za = cta0 ? NA : (int)blockIdx.x - 1;
+  }
+  int zb = 0;
+  bool slots_done = false;
+  uint64_t n_poll = 0, n_node = 0;
+
+  uint32_t backoff = 64;
+  bool node_hot = false;  // the pending node's tiles have all been handed out
+  while (!slots_done || za < NA || zb < NB) {
+    // next slot: sleep in hardware until it fills (bounded while a node is
+    // pending, so the node is still polled about every microsecond)
+    // (a node whose tiles are all handed out is "hot": poll it every ~200 ns)
+    const bool pending = za < NA || zb < NB;
+    const uint32_t hint = pending && node_hot ? 200u : 1000u;
+    if (!slots_done && (pending ? mbar_wait_for(smem_u32(&rs.full[sp.stage]), sp.phase, hint)
+                                : (mbar_wait(smem_u32(&rs.full[sp.stage]), sp.phase), true))) {
+      const int t = rs.tile[sp.stage];
+      if (t >= 0) {
+        for (int f = lane; f < nf; f += 32) {  // nf <= 34
+          const bool mx = f == nf - 1;
+          const double(*w)[NF] = rs.w[sp.stage];
+          const double q0 = combine(w[0][f], w[1][f], mx);
+          const double q1 = combine(w[2][f], w[3][f], mx);
+          const double q2 = combine(w[4][f], w[5][f], mx);
+          const double q3 = combine(w[6][f], w[7][f], mx);
+          st_relaxed(a.tile_part + (int64_t)t * nf + f, combine(combine(q0, q1, mx), combine(q2, q3, mx), mx));
+        }
+      } else {
+        slots_done = true;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&rs.empty[sp.stage]));
+      sp.advance<kSlots>();
+      if (LOOP && slots_done) {
+        bar_arrive_end();  // the CTA may enter the grid barrier now
+        if (it && lane == 0) probe(a, it, 15, global_ns());
+      }
+      continue;
+    }
+    int l, lo, j;
+    if (za < NA) {
+      l = 1;
+      lo = za / g.nodes[1];
+      j = za - lo * g.nodes[1];
+    } else if (zb < NB) {
+      upper_node(g, zb, l, lo, j);
+    } else {
+      continue;
+    }
+    const int oct = g.oct0 + lo;
+    const int nreal = node_real_children(g, oct, l, j);
+    bool advance = nreal == 0;  // unreal node: nothing to do
+    if (!advance) {
+      // every tile under the node handed out?  (local index of its last tile)
+      const long long r0 = octant_real_nodes(g, oct, 0);
+      const long long last = min(((long long)j + 1) << (5 * l), r0) - 1;
+      const int last_lt = (int)((long long)oct * g.M - g.tile0 + last);
+      // (loop kernel, after this CTA's slots: the barrier may already have
+      // re-armed the scheduler, so poll without the hand-out check)
+      node_hot = (LOOP && slots_done) || (int)ld_relaxed_u32(counter) > last_lt;
+      if (node_hot) {
+        ++n_poll;
+        double* child0 = l == 1 ? a.tile_part + ((int64_t)oct * g.M - g.tile0 + (int64_t)j * kFan) * nf
+                                : a.node_part[l - 1] + ((int64_t)lo * g.nodes[l - 1] + (int64_t)j * kFan) * nf;
+        if (LOOP) {  // publish, then count it (readers wait for the count after the grid barrier)
+          advance = try_node<NF, false>(child0, nreal, nf, l1_out + ((int64_t)lo * g.nodes[1] + j) * nf);
+          if (advance && lane == 0) {
+            __threadfence();
+            atomicAdd(&a.ctl->l1_done, 1u);
+          }
+        }
+        else
+          advance = try_node<NF, true>(child0, nreal, nf, a.node_part[l] + ((int64_t)lo * g.nodes[l] + j) * nf);
+        n_node += advance;
+      }
+    }
+    if (advance) {
+      if (za < NA) za += strideA;
+      else ++zb;
+      backoff = 64;
+      node_hot = false;
+    } else if (slots_done) {
+      __nanosleep(backoff);  // pass drained: poll the pending node with a short backoff
+      backoff = min(backoff * 2, 128u);
+    }
+  }
+  if (!LOOP && cta0) {
+    // octant roots (one level-L node per octant; real octants are a prefix)
+    wait_node<NF, false>(a.node_part[g.levels], rank_real_octants(g), nf, rs.root);
+    __syncwarp();
+    for (int f = lane; f < nf; f += 32) a.rank_root[f] = rs.root[f];
+    __syncwarp();
+    if (lane == 0) {
+      if (a.finalize_local)
+        finalize(a.ctl, rs.root, a.c, a.eps, a.max_iters, a.trace, false, a.cond, a.use_cond);
+      __threadfence();
+    }
+  }
+  if (it && lane == 0) {
+    probe(a, it, 8, n_poll);
+    probe(a, it, 9, n_node);
+  }
+}
+
+// The adjacent-pair tree over 32 children (identical association to
+// warp_tree: ((c0+c1)+(c2+c3))+... up to (c0..15)+(c16..31)), evaluated by ONE
+// thread from memory (child i at p[i*stride]; children >= nreal count as
+// 0.0): no shuffles, all loads in flight at once.
+template <bool GLOBAL>
+__device__ __forceinline__ double tree32(const double* p, int64_t stride, int nreal, bool mx) {
+  double v[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i)
+    v[i] = i < nreal ? (GLOBAL ? __ldcg(p + (int64_t)i * stride) : p[(int64_t)i * stride]) : 0.0;
+
+#pragma unroll
+  for (int s2 = 1; s2 < 32; s2 <<= 1)
+#pragma unroll
+    for (int i = 0; i < 32; i += 2 * s2) v[i] = combine(v[i], v[i + s2], mx);
+  return v[0];
+}
+
+// Loop kernel, after the grid barrier of pass `it`: every CTA reduces the
+// levels above 1 from the published level-1 results (l1, [noct][nodes[1]][nf]),
+// the same fixed tree as everywhere else, into root[] -- redundantly, so no
+// further cross-CTA hop is needed.  Each (node, field) pair is one thread's
+// tree32; all kTmaThreads threads call it; scratch is the (idle) stage ring.
+template <int NF>
+__device__ __forceinline__ void loop_upper(const PassArgs& a, const double* l1, double* scratch,
+                                           double (*oroot)[NF], double* root, unsigned it = 0,
+                                           bool from_tiles = false) {
+  const int tid = threadIdx.x;
+  const int nf = 2 * a.c + 2;
+  const Geometry& g = a.g;
+  const int per = g.levels == 3 ? g.nodes[2] : 1;
+  // step 0 (small volumes, no level-1 owners): the level-1 nodes themselves,
+  // from the tile partials the grid barrier published, into shared memory
+  if (from_tiles) {
+    double* l1s = scratch;
+    scratch += (int64_t)g.noct * g.nodes[1] * NF;
+    for (int pr = tid; pr < g.noct * g.nodes[1] * nf; pr += kTmaThreads) {
+      const int z = pr / nf, f = pr - z * nf;
+      const int lo = z / g.nodes[1], j = z - lo * g.nodes[1];
+      const int oct = g.oct0 + lo;
+      const int nreal = (int64_t)oct * g.M < g.T ? node_real_children(g, oct, 1, j) : 0;
+      const double* src = a.tile_part + ((int64_t)oct * g.M - g.tile0 + (int64_t)j * kFan) * nf + f;
+      l1s[(int64_t)z * NF + f] = nreal ? tree32<true>(src, nf, nreal, f == nf - 1) : 0.0;
+    }
+    __syncthreads();
+    l1 = l1s;
+  }
+  const int ls = from_tiles ? NF : nf;  // row stride of the level-1 results
+  // step 1: level-2 nodes (L == 3) or octant roots (L == 2) from level-1 results
+  if (g.levels >= 2) {
+    for (int pr = tid; pr < g.noct * per * nf; pr += kTmaThreads) {
+      const int item = pr / nf, f = pr - item * nf;
+      const int lo = item / per, k = item - lo * per;
+      const int oct = g.oct0 + lo;
+      const int nreal = (int64_t)oct * g.M < g.T ? node_real_children(g, oct, 2, k) : 0;
+      const double* src = l1 + ((int64_t)lo * g.nodes[1] + (int64_t)k * kFan) * ls + f;
+      double r = 0.0;
+      if (nreal) r = from_tiles ? tree32<false>(src, ls, nreal, f == nf - 1) : tree32<true>(src, ls, nreal, f == nf - 1);
+      scratch[(int64_t)item * NF + f] = r;
+    }
+    __syncthreads();
+    if (tid == 0) probe(a, it, 11, global_ns());
+  }
+  // step 2: octant roots
+  for (int pr = tid; pr < g.noct * nf; pr += kTmaThreads) {
+    const int lo = pr / nf, f = pr - lo * nf;
+    const int oct = g.oct0 + lo;
+    double r = 0.0;
+    if ((int64_t)oct * g.M < g.T) {
+      if (g.levels == 1)  // the level-1 node is the octant root
+        r = from_tiles ? l1[(int64_t)lo * ls + f] : __ldcg(l1 + (int64_t)lo * ls + f);
+      else if (g.levels == 2) r = scratch[(int64_t)lo * NF + f];
+      else r = tree32<false>(scratch + (int64_t)lo * per * NF + f, NF, (int)octant_real_nodes(g, oct, 2), f == nf - 1);
+    }
+    oroot[lo][f] = r;
+  }
+  __syncthreads();
+  // step 3: the rank root over the rank's octants (a pair tree over 8 leaves)
+  for (int f = tid; f < nf; f += kTmaThreads) {
+    double v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = (i < g.noct && (int64_t)(g.oct0 + i) * g.M < g.T) ? oroot[i][f] : 0.0;
+    const bool mx = f == nf - 1;
+    root[f] = combine(combine(combine(v[0], v[1], mx), combine(v[2], v[3], mx), mx),
+                      combine(combine(v[4], v[5], mx), combine(v[6], v[7], mx), mx), mx);
+  }
+  __syncthreads();
+}
+
+// -------------------------------------------------------- grid barrier ----
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Called by thread 0 of every CTA after a CTA barrier that follows the CTA's
+// last tile of pass `it`.  The last arriver knows every tile of the pass is
+// finished (so the reduction root and its finalize are published) and every
+// producer has stopped claiming, so it re-arms the tile scheduler and
+// releases generation `it`.  A stuck barrier (which co-residency rules out)
+// times out after 4 s, flags the run, and lets every CTA leave.
+__device__ __forceinline__ bool grid_barrier(Control* ctl, unsigned it, unsigned ncta) {
+  __threadfence();
+  const unsigned prev = atomicAdd(&ctl->bar_count, 1u);
+  if (prev == it * ncta - 1u) {
+    ctl->tile_next[1] = 0u;
+    __threadfence();
+    st_release_u32(&ctl->epoch, it);
+    return true;
+  }
+  const uint64_t t0 = global_ns();
+  while (ld_acquire_u32(&ctl->epoch) < it) {
+    __nanosleep(32);
+    if (global_ns() - t0 > 4000000000ull) {
+      ctl->dead = -3;
+      ctl->done = 1;
+      __threadfence();
+      return false;
+    }
+  }
+  return true;
+}
+
+// Wait (thread 0) until a monotone device counter reaches `target`; false on
+// a 4 s timeout (flags the run like a stuck grid barrier).
+__device__ __forceinline__ bool wait_count(unsigned* ctr, unsigned target) {
+  const uint64_t t0 = global_ns();
+  while (ld_acquire_u32(ctr) < target) {
+    __nanosleep(32);
+    if (global_ns() - t0 > 4000000000ull) return false;
+  }
+  return true;
+}
+
+// Loop kernel, thread 0 of every CTA after the redundant root of pass `it`:
+// the same decisions as finalize_body (core.py:120-131: converged, max_iters,
+// DegenerateClusterError(j), else v_{k+1}) on the CTA's own copy; CTA 0 also
+// publishes them to the control block and the trace.
+__device__ __forceinline__ void finalize_loop(const PassArgs& a, const double* root, unsigned it, double* vsh,
+                                              const double* vnew, int* s_done) {
+  const int c = a.c;
+  if (it == 0) {  // seeded start: v_1 or DegenerateClusterError (core.py:121-123)
+    int dead = -1;
+    for (int j = 0; j < c; ++j)
+      if (root[c + j] == 0.0) {
+        dead = j;
+        break;
+      }
+    if (dead < 0)
+      for (int j = 0; j < c; ++j) vsh[j] = vnew[j];  // root[j] / root[c + j]
+    *s_done = dead >= 0 ? 1 : 0;
+    if (blockIdx.x == 0) {
+      Control* ctl = a.ctl;
+      for (int f = 0; f < 2 * c + 2; ++f) ctl->root[f] = root[f];
+      ctl->dead = dead;
+      if (dead < 0)
+        for (int j = 0; j < c; ++j) ctl->v[j] = vsh[j];
+      ctl->done = dead >= 0 ? 1 : 0;
+    }
+    return;
+  }
+  const int k = (int)it;
+  const double delta = root[2 * c + 1];
+  const bool conv = delta < a.eps;
+  bool done = conv || k >= a.max_iters;
+  int dead = -1;
+  if (!done)
+    for (int j = 0; j < c; ++j)
+      if (root[c + j] == 0.0) {
+        dead = j;
+        done = true;
+        break;
+      }
+  if (!done)
+    for (int j = 0; j < c; ++j) vsh[j] = vnew[j];  // root[j] / root[c + j], computed side by side
+  *s_done = done ? 1 : 0;
+  if (blockIdx.x == 0) {
+    Control* ctl = a.ctl;
+    for (int f = 0; f < 2 * c + 2; ++f) {
+      ctl->root[f] = root[f];
+      a.rank_root[f] = root[f];
+    }
+    ctl->iter = k;
+    a.trace[k - 1] = root[2 * c];
+    ctl->delta = delta;
+    ctl->converged = conv ? 1 : 0;
+    ctl->dead = dead;
+    if (!done)
+      for (int j = 0; j < c; ++j) ctl->v[j] = vsh[j];
+    ctl->done = done ? 1 : 0;
+  }
+}
+
+// Loop kernel, multi-rank: publish this rank's root (in root[], every CTA
+// has it) to every rank's mailbox, wait for all ranks' roots of this pass in
+// the local mailbox, and replace root[] by the rank-ordered pair tree over
+// them -- the same tree the octants use (tree_model.combine_ranks), so the
+// global root is the single-rank root bit for bit.  All threads call it.
+// Returns false on a 4 s timeout (a peer died): the run is flagged.
+__device__ __forceinline__ bool exchange_roots(const PassArgs& a, double* root, unsigned gen) {
+  const int tid = threadIdx.x;
+  const int nf = 2 * a.c + 2;
+  const int par = gen & 1;
+  const unsigned tag = (a.mb_run << 16) | (gen & 0xffffu);
+  if (blockIdx.x == 0 && tid < a.mb_ranks) {  // thread p writes rank p's copy (NVLink stores)
+    Mailbox* mb = a.mbox_peer[tid];
+    for (int f = 0; f < nf; ++f) mb->root[par][a.mb_rank][f] = root[f];
+    __threadfence_system();
+    st_release_sys_u32(&mb->tag[par][a.mb_rank], tag);
+  }
+  __shared__ int s_ok;
+  if (tid == 0) {
+    s_ok = 1;
+    const uint64_t t0 = global_ns();
+    for (int r = 0; r < a.mb_ranks && s_ok; ++r)
+      while (ld_acquire_sys_u32(&a.mbox_local->tag[par][r]) != tag) {
+        __nanosleep(64);
+        if (global_ns() - t0 > 4000000000ull) {
+          s_ok = 0;
+          break;
+        }
+      }
+  }
+  __syncthreads();
+  if (!s_ok) return false;
+  for (int f = tid; f < nf; f += kTmaThreads) {
+    double v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = i < a.mb_ranks ? ld_relaxed_sys(&a.mbox_local->root[par][i][f]) : 0.0;
+    const bool mx = f == nf - 1;
+    root[f] = combine(combine(combine(v[0], v[1], mx), combine(v[2], v[3], mx), mx),
+                      combine(combine(v[4], v[5], mx), combine(v[6], v[7], mx), mx), mx);
+  }
+  __syncthreads();
+  return true;
+}
+
+}  // namespace fcm
