@@ -115,6 +115,7 @@ struct fcm_plan {
   int l2_mode = 1;  // 0 never keep x/u in L2, 1 when they fit (default), 2 always
   int profile = 0;  // record the loop kernel's per-CTA timeline
   int seed_pass = 1;  // loop kernel generates the seeded u_0 as its pass 0
+  int recompute = 0;  // loop kernel: "effective" mode, passes >= 2 stream x only
   unsigned run_counter = 0;  // fcm_run calls (mailbox tags); identical on every rank
   bool p2p_ready = false;    // multi-process ranks: peer mailboxes mapped (fcm_connect_peers)
   Mailbox* peer_mbox[kOctants] = {};
@@ -689,6 +690,7 @@ int fcm_set_option(fcm_plan* p, int32_t key, int64_t value) {
     case FCM_OPT_LOOP: p->use_loop = value ? 1 : 0; return FCM_OK;
     case FCM_OPT_PROFILE: p->profile = value ? 1 : 0; return FCM_OK;
     case FCM_OPT_SEED_PASS: p->seed_pass = value ? 1 : 0; return FCM_OK;
+    case FCM_OPT_RECOMPUTE: p->recompute = value ? 1 : 0; return FCM_OK;
     case FCM_OPT_L2:
       if (value < 0 || value > 2) return FCM_E_ARG;
       p->l2_mode = (int)value;
@@ -831,6 +833,9 @@ int fcm_run(fcm_plan* p, double m, double eps, int32_t max_iters, double* v_out,
       CK(cudaSetDevice(s.device));
       PassArgs a = make_args(p, s, 1, eps, max_iters);
       a.seed_pass = seed_pass ? 1 : 0;
+      // recompute needs the intensity set, tracked by the seeded pass 0
+      a.recompute = (p->recompute && seed_pass && p->xkind == XK_U8 && p->mode == MODE_M2 && p->c <= 8 &&
+                     p->variant == 0) ? 1 : 0;
       a.mb_ranks = p->nranks;
       a.mb_rank = p->nshards > 1 ? i : p->rank;
       a.mb_run = run ? run : 1;

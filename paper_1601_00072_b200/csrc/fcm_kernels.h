@@ -35,6 +35,7 @@ struct PassArgs {
   int keep_l2;            // 1: x + u fit in L2 -> evict_last loads/stores (next pass hits L2)
   double* l1_buf;         // loop kernel: level-1 node results [3][noct][nodes[1]][nf] (generation mod 3)
   int seed_pass;          // loop kernel: 1 = run the seeded start as pass 0 (no prologue kernel)
+  int recompute;          // loop kernel: passes >= 2 stream x only; delta from the intensity tables
   int mb_ranks;           // loop kernel: ranks exchanging roots through mailboxes (1 = none)
   int mb_rank;            // this rank's slot
   unsigned mb_run;        // run tag (fcm_run counter, identical on every rank)

@@ -91,6 +91,9 @@ __global__ void __launch_bounds__(kTmaThreads, 2) loop_tma_kernel(PassArgs a) {
   __shared__ double oroot[kOctants][NF];
   __shared__ double vsh[C];
   __shared__ double vnew[C];
+  __shared__ double vprev[C];     // recompute mode: centers of the previous pass
+  __shared__ double sdelta;       // recompute mode: delta of this pass from the tables
+  __shared__ uint32_t spresent[8];
   __shared__ int s_done;
   const int tid = threadIdx.x;
   const int c = C <= 8 ? C : a.c;
@@ -104,6 +107,10 @@ __global__ void __launch_bounds__(kTmaThreads, 2) loop_tma_kernel(PassArgs a) {
   // small volumes (<= 1024 tiles): no level-1 owners -- every CTA reduces
   // the level-1 nodes itself after the grid barrier (one hop less per pass)
   const bool from_tiles = a.g.tiles_local <= kSmallTiles;
+  // recompute mode (SURVEY 8(d) "effective"): passes >= 2 stream x only;
+  // u_{k-1} is never read back -- delta_k = max over the intensities present
+  // of |u_k(b) - u_{k-1}(b)| from the two pass tables (fp64, exact)
+  const bool recomp = a.recompute && MODE == MODE_LUT2 && sizeof(XT) == 1;
   unsigned l1_real = 0;  // real level-1 nodes of this rank (published once per pass)
   if (!from_tiles)
     for (int lo = 0; lo < a.g.noct; ++lo) l1_real += (unsigned)octant_real_nodes(a.g, a.g.oct0 + lo, 1);
@@ -120,7 +127,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) loop_tma_kernel(PassArgs a) {
     if (tid >= kThreads) {
       if (tid == kProducerTid) {
         fence_proxy_async_global();
-        const int n = tma_produce<XT, C, MODE>(a, smem, ps, &a.ctl->tile_next[1], it, it == 0);
+        const int n = tma_produce<XT, C, MODE>(a, smem, ps, &a.ctl->tile_next[1], it, it == 0 || (recomp && it >= 2));
         probe(a, it, 1, global_ns());
         probe(a, it, 4, (uint64_t)n);
         unsigned smid;
@@ -145,7 +152,14 @@ __global__ void __launch_bounds__(kTmaThreads, 2) loop_tma_kernel(PassArgs a) {
         double lwx[C], lwb[C], ljb = 0.0;
         if (LUT) tma_build_lut<C>(smem + L::kLutOff, v, c, pw, lwx, lwb, ljb);
         if (MODE == MODE_LUT2) tma_build_lut2<C>(smem + L::kLutOff, v);
-        tma_consume<XT, C, MODE>(a, smem, ps, rs, sp, v, pw, lwx, lwb, ljb, it);
+        if (recomp && it >= 2) {
+          if (tid < 8) spresent[tid] = __ldcg(&a.ctl->present[tid]);
+          red_sync<true>();
+          table_delta<C>(v, vprev, spresent, c, &sdelta);
+          tma_consume<XT, C, MODE, true>(a, smem, ps, rs, sp, v, pw, lwx, lwb, ljb, it);
+        } else {
+          tma_consume<XT, C, MODE>(a, smem, ps, rs, sp, v, pw, lwx, lwb, ljb, it);
+        }
         if (tid == 0) probe(a, it, 2, global_ns());
       }
       bar_sync_end();
@@ -161,7 +175,8 @@ __global__ void __launch_bounds__(kTmaThreads, 2) loop_tma_kernel(PassArgs a) {
     }
     __syncthreads();
     if (s_done) break;
-    loop_upper<NF>(a, l1, reinterpret_cast<double*>(smem), oroot, rs.root, it, from_tiles);
+    loop_upper<NF>(a, l1, reinterpret_cast<double*>(smem), oroot, rs.root, it, from_tiles,
+                   (recomp && it >= 2) ? sdelta : 0.0);
     if (tid == 0) probe(a, it, 10, global_ns());
     if (a.mb_ranks > 1 && !exchange_roots(a, rs.root, gen)) {
       if (tid == 0) {
@@ -173,6 +188,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) loop_tma_kernel(PassArgs a) {
     if (tid < c) vnew[tid] = rs.root[tid] / rs.root[c + tid];  // the c divisions side by side
     __syncthreads();
     if (tid == 0) {
+      for (int j = 0; j < c; ++j) vprev[j] = vsh[j];  // the centers this pass used
       finalize_loop(a, rs.root, it, vsh, vnew, &s_done);
       probe(a, it, 14, global_ns());
     }

@@ -483,6 +483,12 @@ __device__ __forceinline__ void tma_consume_seed(const PassArgs& a, uint8_t* sme
   double acc[NS];
 #pragma unroll
   for (int s = 0; s < NS; ++s) acc[s] = 0.0;
+  // recompute mode: which intensities occur (256 bits per thread, OR-reduced
+  // into ctl->present at the end of the pass)
+  const bool track = a.recompute && sizeof(XT) == 1;
+  uint32_t pm[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) pm[k] = 0u;
   for (;;) {
     mbar_wait(bar0 + 8u * ps.stage, ps.phase);
     const StageMeta mt = meta[ps.stage];
@@ -491,6 +497,13 @@ __device__ __forceinline__ void tma_consume_seed(const PassArgs& a, uint8_t* sme
       __syncwarp();
       if ((tid & 31) == 0) mbar_arrive(bar0 + 8u * (S + ps.stage));
       ps.advance<S>();
+      if (track) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t w = __reduce_or_sync(0xffffffffu, pm[k]);
+          if ((tid & 31) == 0 && w) atomicOr(&a.ctl->present[k], w);
+        }
+      }
       mbar_wait(smem_u32(&rs.empty[sp.stage]), sp.phase ^ 1u);
       if (tid == 0) rs.tile[sp.stage] = -1;
       __syncwarp();
@@ -504,6 +517,16 @@ __device__ __forceinline__ void tma_consume_seed(const PassArgs& a, uint8_t* sme
       const uint32_t w = *reinterpret_cast<const uint32_t*>(st + tid * 4);
 #pragma unroll
       for (int q = 0; q < 4; ++q) xd[q] = u8_to_f64((w >> (8 * q)) & 0xffu);
+      if (track) {
+        const int64_t nv = a.g.n_local - i0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const uint32_t b = (w >> (8 * q)) & 0xffu;
+          const uint32_t bit = q < nv ? 1u << (b & 31u) : 0u;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) pm[k] |= (b >> 5) == (uint32_t)k ? bit : 0u;
+        }
+      }
     } else {
       const double2 p0 = *reinterpret_cast<const double2*>(st + tid * 32);
       const double2 p1 = *reinterpret_cast<const double2*>(st + tid * 32 + 16);
@@ -542,7 +565,7 @@ __device__ __forceinline__ void tma_consume_seed(const PassArgs& a, uint8_t* sme
   }
 }
 
-template <typename XT, int C, int MODE>
+template <typename XT, int C, int MODE, bool XONLY = false>
 __device__ __forceinline__ void tma_consume(const PassArgs& a, uint8_t* smem, Pipe& ps,
                                             RedSlots<2 * C + 2>& rs, Pipe& sp, const double* v,
                                             const Powers& pw, const double* lwx = nullptr,
@@ -604,8 +627,10 @@ __device__ __forceinline__ void tma_consume(const PassArgs& a, uint8_t* smem, Pi
     }
     float4 uo[C];
 #pragma unroll
-    for (int j = 0; j < C; ++j)
-      if (j < c) uo[j] = *reinterpret_cast<const float4*>(st + L::kXBytes + j * L::kUBytes + tid * 16);
+    for (int j = 0; j < C; ++j) {
+      uo[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (j < c && !XONLY) uo[j] = *reinterpret_cast<const float4*>(st + L::kXBytes + j * L::kUBytes + tid * 16);
+    }
     __syncwarp();
     if ((tid & 31) == 0) mbar_arrive(bar0 + 8u * (S + ps.stage));
     ps.advance<S>();
@@ -644,7 +669,12 @@ __device__ __forceinline__ void tma_consume(const PassArgs& a, uint8_t* smem, Pi
           e[2 * k] = w2.x;
           e[2 * k + 1] = w2.y;
         }
-        m2_fold<C>(xd[q], e, e[C], uq, nq, acc, dmax_hi, valid);
+        if (XONLY) {  // recompute mode: delta comes from the tables, not from u_{k-1}
+          uint32_t none = 0;
+          m2_fold<C>(xd[q], e, e[C], uq, nq, acc, none, valid);
+        } else {
+          m2_fold<C>(xd[q], e, e[C], uq, nq, acc, dmax_hi, valid);
+        }
       } else if (MODE == MODE_M2 && sizeof(XT) == 1 && C <= 8)
         voxel_m2_u8<C>(xd[q], v, uq, nq, acc, dmax_hi, valid);
       else

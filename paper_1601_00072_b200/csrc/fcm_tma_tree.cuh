@@ -45,6 +45,37 @@ __device__ __forceinline__ void wait_node(double* child0, int nreal, int nf, dou
   while (!try_node<NF, GLOBAL_OUT>(child0, nreal, nf, out)) __nanosleep(32);
 }
 
+// Recompute mode, consumer threads (thread b = intensity b): this pass's
+// delta = max over the intensities present in the rank of
+// max_j |u_k(b)_j - u_{k-1}(b)_j|, both from the m == 2 product form in
+// fp64 (v = v_k, vprev = v_{k-1}).  max is order-independent, so every CTA
+// gets the same value.  Ends with a consumer barrier.
+template <int C>
+__device__ __forceinline__ void table_delta(const double* v, const double* vprev, const uint32_t* present, int c,
+                                            double* out) {
+  __shared__ double wmax[kWarps];
+  const int b = threadIdx.x;
+  double d = 0.0;
+  if ((present[b >> 5] >> (b & 31)) & 1u) {
+    double uk[C], up[C], ok, op;
+    m2_membership<C>((double)b, v, uk, ok);
+    m2_membership<C>((double)b, vprev, up, op);
+#pragma unroll
+    for (int j = 0; j < C; ++j)
+      if (j < c) d = fmax(d, fabs(uk[j] - up[j]));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) d = fmax(d, __shfl_xor_sync(0xffffffffu, d, o));
+  if ((b & 31) == 0) wmax[b >> 5] = d;
+  red_sync<true>();
+  if (b == 0) {
+    double m = 0.0;
+    for (int w = 0; w < kWarps; ++w) m = fmax(m, wmax[w]);
+    *out = m;
+  }
+  red_sync<true>();
+}
+
 // Node k of CTA 0's upper-level list -- levels 2..L, octant by octant, each
 // octant's level-2 nodes before its level-3 node -- as (level, octant, j).
 __device__ __forceinline__ void upper_node(const Geometry& g, int k, int& l, int& lo, int& j) {
@@ -222,7 +253,7 @@ __device__ __forceinline__ double tree32(const double* p, int64_t stride, int nr
 template <int NF>
 __device__ __forceinline__ void loop_upper(const PassArgs& a, const double* l1, double* scratch,
                                            double (*oroot)[NF], double* root, unsigned it = 0,
-                                           bool from_tiles = false) {
+                                           bool from_tiles = false, double extra_delta = 0.0) {
   const int tid = threadIdx.x;
   const int nf = 2 * a.c + 2;
   const Geometry& g = a.g;
@@ -281,6 +312,7 @@ __device__ __forceinline__ void loop_upper(const PassArgs& a, const double* l1, 
     const bool mx = f == nf - 1;
     root[f] = combine(combine(combine(v[0], v[1], mx), combine(v[2], v[3], mx), mx),
                       combine(combine(v[4], v[5], mx), combine(v[6], v[7], mx), mx), mx);
+    if (mx) root[f] = fmax(root[f], extra_delta);  // recompute mode: the table delta
   }
   __syncthreads();
 }
