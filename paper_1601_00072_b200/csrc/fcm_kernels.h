@@ -44,7 +44,7 @@ struct PassArgs {
   uint64_t* prof;         // loop-kernel timeline [prof_passes][grid][kProbeSlots] or null
   int prof_passes;
 };
-constexpr int kProbeSlots = 16;
+constexpr int kProbeSlots = 20;
 
 struct FinalizeArgs {
   const double* roots[kOctants];  // rank r's reduction root (peer, local or NCCL-gathered)

@@ -116,6 +116,10 @@ __global__ void __launch_bounds__(kTmaThreads, 2) loop_tma_kernel(PassArgs a) {
     for (int lo = 0; lo < a.g.noct; ++lo) l1_real += (unsigned)octant_real_nodes(a.g, a.g.oct0 + lo, 1);
   Pipe ps, sp;
   unsigned gen = 0;  // grid-barrier generations
+  // monotone tile scheduler: every producer makes exactly one failing claim
+  // per pass, so pass p hands out [p(T+G), p(T+G)+T) -- no per-pass reset
+  unsigned sched = 0;
+  const unsigned sched_step = (unsigned)a.g.tiles_local + gridDim.x;
   __syncthreads();
   for (unsigned it = a.seed_pass ? 0u : 1u; !s_done && it <= (unsigned)a.max_iters; ++it) {
     if (tid == 0) probe(a, it, 0, global_ns());
@@ -127,7 +131,8 @@ __global__ void __launch_bounds__(kTmaThreads, 2) loop_tma_kernel(PassArgs a) {
     if (tid >= kThreads) {
       if (tid == kProducerTid) {
         fence_proxy_async_global();
-        const int n = tma_produce<XT, C, MODE>(a, smem, ps, &a.ctl->tile_next[1], it, it == 0 || (recomp && it >= 2));
+        const int n = tma_produce<XT, C, MODE>(a, smem, ps, &a.ctl->tile_next[1], it, it == 0 || (recomp && it >= 2),
+                                                     sched);
         probe(a, it, 1, global_ns());
         probe(a, it, 4, (uint64_t)n);
         unsigned smid;
@@ -137,7 +142,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) loop_tma_kernel(PassArgs a) {
       if ((tid >> 5) == kReducerWarp) {
         // slots first (then arrive at the pass-end barrier), owned level-1
         // nodes after -- overlapping the grid barrier
-        tma_reduce<C, true>(a, rs, sp, &a.ctl->tile_next[1], l1, it, from_tiles);
+        tma_reduce<C, true>(a, rs, sp, &a.ctl->tile_next[1], l1, it, from_tiles, sched);
         if ((tid & 31) == 0) probe(a, it, 7, global_ns());
       } else {
         bar_sync_end();
@@ -165,8 +170,9 @@ __global__ void __launch_bounds__(kTmaThreads, 2) loop_tma_kernel(PassArgs a) {
       bar_sync_end();
     }
     gen = gnext;
+    sched += sched_step;
     if (tid == 0) {
-      if (!grid_barrier(a.ctl, gen, gridDim.x) || !wait_count(&a.ctl->l1_done, gen * l1_real)) {
+      if (!grid_barrier(a.ctl, gen, gridDim.x) || (l1_real && !wait_count(&a.ctl->l1_done, gen * l1_real))) {
         a.ctl->dead = -3;  // a stuck CTA (cannot happen with co-resident CTAs): flag the run
         a.ctl->done = 1;
         s_done = 1;
@@ -194,6 +200,8 @@ __global__ void __launch_bounds__(kTmaThreads, 2) loop_tma_kernel(PassArgs a) {
     }
     __syncthreads();
   }
+  // leave the scheduler as the run found it (every claim is behind the last barrier)
+  if (blockIdx.x == 0 && tid == 0) a.ctl->tile_next[1] = 0u;
 }
 
 template <typename XT, int C, int MODE>

@@ -344,7 +344,7 @@ __device__ __forceinline__ void probe(const PassArgs& a, unsigned it, int k, uin
 // ring, then post the end-of-pass marker.
 template <typename XT, int C, int MODE>
 __device__ __forceinline__ int tma_produce(const PassArgs& a, uint8_t* smem, Pipe& ps, unsigned* counter,
-                                           unsigned it = 0, bool x_only = false) {
+                                           unsigned it = 0, bool x_only = false, unsigned base = 0) {
   using L = TmaLayout<XT, C, MODE>;
   constexpr int S = L::kStages;
   const uint32_t bar0 = smem_u32(smem + L::kBarOff);
@@ -357,7 +357,7 @@ __device__ __forceinline__ int tma_produce(const PassArgs& a, uint8_t* smem, Pip
   const int ntiles = a.g.tiles_local;
   int claimed = 0;
   for (;;) {
-    const int lt = (int)atomicAdd(counter, 1u);
+    const int lt = (int)(atomicAdd(counter, 1u) - base);  // (mod 2^32: a monotone counter)
     if (lt >= ntiles) {
       mbar_wait(bar0 + 8u * (S + ps.stage), ps.phase ^ 1u);
       meta[ps.stage].tile = -1;

@@ -106,7 +106,7 @@ __device__ __forceinline__ void upper_node(const Geometry& g, int k, int& l, int
 template <int C, bool LOOP>
 __device__ __forceinline__ void tma_reduce(const PassArgs& a, RedSlots<2 * C + 2>& rs, Pipe& sp,
                                            const unsigned* counter, double* l1_out, unsigned it = 0,
-                                           bool no_owners = false) {
+                                           bool no_owners = false, unsigned base = 0) {
   constexpr int NF = 2 * C + 2;
   const int lane = threadIdx.x & 31;
   const int nf = 2 * a.c + 2;
@@ -182,7 +182,7 @@ __device__ __forceinline__ void tma_reduce(const PassArgs& a, RedSlots<2 * C + 2
       const int last_lt = (int)((long long)oct * g.M - g.tile0 + last);
       // (loop kernel, after this CTA's slots: the barrier may already have
       // re-armed the scheduler, so poll without the hand-out check)
-      node_hot = (LOOP && slots_done) || (int)ld_relaxed_u32(counter) > last_lt;
+      node_hot = (LOOP && slots_done) || (int)(ld_relaxed_u32(counter) - base) > last_lt;
       if (node_hot) {
         ++n_poll;
         double* child0 = l == 1 ? a.tile_part + ((int64_t)oct * g.M - g.tile0 + (int64_t)j * kFan) * nf
@@ -260,6 +260,7 @@ __device__ __forceinline__ void loop_upper(const PassArgs& a, const double* l1, 
   const int per = g.levels == 3 ? g.nodes[2] : 1;
   // step 0 (small volumes, no level-1 owners): the level-1 nodes themselves,
   // from the tile partials the grid barrier published, into shared memory
+  if (tid == 0) probe(a, it, 16, global_ns());
   if (from_tiles) {
     double* l1s = scratch;
     scratch += (int64_t)g.noct * g.nodes[1] * NF;
@@ -272,6 +273,7 @@ __device__ __forceinline__ void loop_upper(const PassArgs& a, const double* l1, 
       l1s[(int64_t)z * NF + f] = nreal ? tree32<true>(src, nf, nreal, f == nf - 1) : 0.0;
     }
     __syncthreads();
+    if (tid == 0) probe(a, it, 17, global_ns());
     l1 = l1s;
   }
   const int ls = from_tiles ? NF : nf;  // row stride of the level-1 results
@@ -333,17 +335,14 @@ __device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
 // producer has stopped claiming, so it re-arms the tile scheduler and
 // releases generation `it`.  A stuck barrier (which co-residency rules out)
 // times out after 4 s, flags the run, and lets every CTA leave.
-__device__ __forceinline__ bool grid_barrier(Control* ctl, unsigned it, unsigned ncta) {
+__device__ __forceinline__ bool grid_barrier(Control* ctl, unsigned gen, unsigned ncta) {
+  // release this CTA's writes (tile partials, u), arrive, then wait until the
+  // monotone count reaches gen * ncta -- no last-arriver hop, no reset
   __threadfence();
-  const unsigned prev = atomicAdd(&ctl->bar_count, 1u);
-  if (prev == it * ncta - 1u) {
-    ctl->tile_next[1] = 0u;
-    __threadfence();
-    st_release_u32(&ctl->epoch, it);
-    return true;
-  }
+  atomicAdd(&ctl->bar_count, 1u);
+  const unsigned target = gen * ncta;
   const uint64_t t0 = global_ns();
-  while (ld_acquire_u32(&ctl->epoch) < it) {
+  while ((int)(ld_acquire_u32(&ctl->bar_count) - target) < 0) {
     __nanosleep(32);
     if (global_ns() - t0 > 4000000000ull) {
       ctl->dead = -3;

@@ -198,12 +198,13 @@ class FcmPlan:
     def profile(self) -> np.ndarray:
         """Loop-kernel timeline of the last run (FCM_OPT_PROFILE): array [pass, cta, slot]
         with slots 0 start, 1 claims done, 2 consumers done, 3 barrier released (ns), 4 tiles."""
-        cap = 64 * 8 * 1024 * 16
+        slots = 20  # kProbeSlots (fcm_kernels.h)
+        cap = 64 * 8 * 1024 * slots
         buf = np.zeros(cap, dtype=np.uint64)
         passes, grid = ctypes.c_int32(), ctypes.c_int32()
         check(lib().fcm_last_profile(self._h, ptr(buf), cap, ctypes.byref(passes), ctypes.byref(grid)),
               self._h, "fcm_last_profile")
-        return buf[: passes.value * grid.value * 16].reshape(passes.value, grid.value, 16)
+        return buf[: passes.value * grid.value * slots].reshape(passes.value, grid.value, slots)
 
     # -- label statistics (metrics on the device) ------------------------
     def confusion(self, ref_labels: np.ndarray, c_ref: int) -> np.ndarray:

@@ -60,8 +60,12 @@ print("consumers done max", (int(P[1, :, 2].max()) - b0) / 1e3, "reducers done m
       "barrier released", (int(P[1, :, 3].max()) - b0) / 1e3, "root done max", (int(P[1, :, 14].max()) - b0) / 1e3,
       "next start max", (int(P[2, :, 0].max()) - b0) / 1e3)
 
+def mn0(j, it=1):
+    return (np.median(P[it, :, j].astype(np.int64)) - int(P[it, :, 0].min())) / 1e3
+
 def mx(j, it=1):
     return (int(P[it, :, j].max()) - int(P[it, :, 0].min())) / 1e3
+print("pass 2 upper (max/median over CTAs): start", mx(16), mn0(16), "step0", mx(17), mn0(17), "step1", mx(11), mn0(11))
 print("pass 2 chain (max over CTAs, us from pass start): consumers", mx(2), "reducers", mx(7), "barrier", mx(3),
       "upper step1", mx(11), "upper done", mx(10), "finalize", mx(14), "next start", (int(P[2, :, 0].max()) - int(P[1, :, 0].min())) / 1e3)
 
