@@ -210,23 +210,43 @@ def run_ours(args, rank, world, local_rank, dist):
     # (FCM_BENCH_DIST_BACKEND=gloo, used to run N ranks on one test GPU)
     tdev = "cuda" if (world > 1 and dist.get_backend() == "nccl") else "cpu"
     device = local_rank % max(1, _device_count()) if os.environ.get("FCM_BENCH_DEVICE_MODULO") else local_rank
-    nccl_id = None
-    if world > 1 and args.transport == "nccl":
-        import torch
-        buf = torch.zeros(128, dtype=torch.uint8, device=tdev)
-        if rank == 0:
-            buf.copy_(torch.frombuffer(bytearray(pkg.FcmPlan.nccl_unique_id()), dtype=torch.uint8))
-        dist.broadcast(buf, 0)
-        nccl_id = bytes(buf.cpu().numpy().tobytes())
-    plan = pkg.FcmPlan.for_rank(n, c, _lib.FCM_X_U8, device, world, rank, nccl_id)
-    if world > 1 and args.transport == "p2p":
-        # fused exchange: map every rank's root mailbox (CUDA IPC over NVLink);
-        # the loop kernel then writes the 2c+2 roots straight into the peers
-        import torch
-        mine = torch.frombuffer(bytearray(plan.mailbox_handle()), dtype=torch.uint8).to(tdev)
-        allh = [torch.zeros_like(mine) for _ in range(world)]
-        dist.all_gather(allh, mine)
-        plan.connect_peers(b"".join(bytes(t.cpu().numpy().tobytes()) for t in allh), world)
+    def make_plan(transport):
+        nccl_id = None
+        if world > 1 and transport == "nccl":
+            import torch
+            buf = torch.zeros(128, dtype=torch.uint8, device=tdev)
+            if rank == 0:
+                buf.copy_(torch.frombuffer(bytearray(pkg.FcmPlan.nccl_unique_id()), dtype=torch.uint8))
+            dist.broadcast(buf, 0)
+            nccl_id = bytes(buf.cpu().numpy().tobytes())
+        p = pkg.FcmPlan.for_rank(n, c, _lib.FCM_X_U8, device, world, rank, nccl_id)
+        if world > 1 and transport == "p2p":
+            # fused exchange: map every rank's root mailbox (CUDA IPC over NVLink);
+            # the loop kernel then writes the 2c+2 roots straight into the peers
+            import torch
+            ok = 1
+            try:
+                mine = torch.frombuffer(bytearray(p.mailbox_handle()), dtype=torch.uint8).to(tdev)
+            except Exception as e:  # noqa: BLE001 -- agreed on below
+                print(f"[bench] rank {rank}: mailbox handle failed: {e}", file=sys.stderr)
+                ok, mine = 0, torch.zeros(64, dtype=torch.uint8, device=tdev)
+            allh = [torch.zeros_like(mine) for _ in range(world)]
+            dist.all_gather(allh, mine)
+            if ok:
+                try:
+                    p.connect_peers(b"".join(bytes(t.cpu().numpy().tobytes()) for t in allh), world)
+                except Exception as e:  # noqa: BLE001
+                    print(f"[bench] rank {rank}: peer mapping failed: {e}", file=sys.stderr)
+                    ok = 0
+            flag = torch.tensor([ok], dtype=torch.int32, device=tdev)
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+            if int(flag.item()) == 0:  # every rank falls back together: NCCL all-gather per pass
+                p.close()
+                args.transport = "nccl"
+                return make_plan("nccl")
+        return p
+
+    plan = make_plan(args.transport)
     x = np.ascontiguousarray(x_full[plan.voxel0:plan.voxel0 + plan.n_local])
     del x_full
     plan.upload_pixels(x)
@@ -383,8 +403,9 @@ def run_ours(args, rank, world, local_rank, dist):
             "n_voxels": n, "c": c, "m": m, "epsilon": eps, "seed": 0,
             "iterations_per_solve": iters[0],
             "step": "one fcm_run: device seeded start + fused passes to convergence",
-            "l2": ("inputs larger than L2 (x u8 + the c fp32 membership planes, 3.4 GB per pass at C4); no flush needed"
-                   if n * (1 + 4 * c) > 126e6 else
+            "l2": (f"inputs larger than L2 (x u8 + the c fp32 membership planes, "
+                   f"{plan.n_local * (1 + 4 * c) / 1e9:.2f} GB per pass per GPU); no flush needed"
+                   if plan.n_local * (1 + 4 * c) > 126e6 else
                    "working set (x + memberships) fits L2 and is kept there between passes (evict_last policy); not flushed"),
             "parallelism": (f"voxel shards x{world}, 2c+2 roots per iteration written into every rank's "
                             f"mailbox by the loop kernel (NVLink peer stores)" if args.transport == "p2p" else
