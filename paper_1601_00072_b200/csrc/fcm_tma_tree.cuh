@@ -358,7 +358,7 @@ __device__ __forceinline__ bool grid_barrier(Control* ctl, unsigned gen, unsigne
 // a 4 s timeout (flags the run like a stuck grid barrier).
 __device__ __forceinline__ bool wait_count(unsigned* ctr, unsigned target) {
   const uint64_t t0 = global_ns();
-  while (ld_acquire_u32(ctr) < target) {
+  while ((int)(ld_acquire_u32(ctr) - target) < 0) {  // modular: counts may wrap on very long runs
     __nanosleep(32);
     if (global_ns() - t0 > 4000000000ull) return false;
   }
