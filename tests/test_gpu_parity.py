@@ -326,8 +326,9 @@ def test_mailbox_exchange_loop_kernels_bitwise(devices, c, m):
     assert ua.tobytes() == ub.tobytes() and np.array_equal(la, lb)
 
 
+@pytest.mark.parametrize("shards", [1, 4])
 @pytest.mark.parametrize("name", ["C1", "phantom_c4", "small4_seq", "mixture_c3", "zero_c2", "twopop_c2", "cap1_c2"])
-def test_recompute_mode_matches_canonical(name):
+def test_recompute_mode_matches_canonical(name, shards):
     """Recompute ("effective") mode: passes >= 2 never read u_{k-1}; delta is
     taken between the fp64 intensity tables over the intensities present.
     Same iterations, centers, objective trace, memberships and labels as the
@@ -339,8 +340,10 @@ def test_recompute_mode_matches_canonical(name):
         pytest.skip("recompute mode is the m == 2 table path")
     x = r["x"].astype(np.uint8)
 
-    def solve(recompute):
-        with pkg.FcmPlan(x.shape[0], r["c"], _lib.FCM_X_U8) as plan:
+    def solve(recompute, nsh=1):
+        # several shards on one GPU: concurrent loop kernels, per-shard
+        # intensity sets, deltas max-combined through the mailboxes
+        with pkg.FcmPlan(x.shape[0], r["c"], _lib.FCM_X_U8, [0] * nsh) as plan:
             plan.upload_pixels(x)
             plan.init_membership(r["seed"])
             plan.set_option(_lib.FCM_OPT_RECOMPUTE, recompute)
@@ -349,7 +352,7 @@ def test_recompute_mode_matches_canonical(name):
         return out, u, lab
 
     (va, ta, ka, ca), ua, la = solve(0)
-    (vb, tb, kb, cb), ub, lb = solve(1)
+    (vb, tb, kb, cb), ub, lb = solve(1, shards)
     assert ka == kb == r["iterations"] and ca == cb
     assert va.tobytes() == vb.tobytes() and ta.tobytes() == tb.tobytes()
     assert ua.tobytes() == ub.tobytes() and np.array_equal(la, lb)
