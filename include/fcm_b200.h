@@ -156,6 +156,18 @@ int fcm_run(fcm_plan* plan, double m, double epsilon, int32_t max_iters, double*
  * of the plan's voxel range.  Either pointer may be NULL. */
 int fcm_download(fcm_plan* plan, double* u_aos_out, int32_t* labels_out);
 
+/* fcm_download for uint8 plans without moving n*c doubles over PCIe: u_final
+ * and the labels depend only on (x_i, v_final), so the epilogue is evaluated
+ * for the 256 intensities (same kernel: bit-identical rows), 256*(8c+4) bytes
+ * are copied back, and `nthreads` host threads (<= 0: all cores) expand the
+ * rows along x_host -- the same pixels the plan uploaded (its voxel range) --
+ * with streaming stores.  Output identical to fcm_download; the device labels
+ * are still written for fcm_label_confusion / fcm_mask_overlap.
+ * FCM_E_ARG for float64 plans.  Reference: core.py:132 / defuzzify core.py:94-102
+ * (the FcmResult arrays); no reference counterpart for the table itself. */
+int fcm_download_table(fcm_plan* plan, const uint8_t* x_host, double* u_aos_out, int32_t* labels_out,
+                       int32_t nthreads);
+
 /* Label statistics of the last solve, counted on the device from the labels
  * fcm_download left there (metrics.py:46-97: Dice and match_clusters need
  * only these integers).  ref_labels: int32 class per voxel of the plan's

@@ -13,7 +13,10 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
+
+#include <emmintrin.h>
 
 #include <nccl.h>
 
@@ -70,6 +73,9 @@ struct Shard {
   double* u0_aos = nullptr;
   double* tile_part = nullptr;
   double* node_part[kMaxLevels + 1] = {};  // level l >= 1: [noct][nodes[l]][nf]
+  uint8_t* tab_x = nullptr;                // fcm_download_table: intensities 0..255
+  double* tab_u = nullptr;                 //   their fp64 membership rows
+  int32_t* tab_l = nullptr;                //   and labels
   double* l1_buf = nullptr;                // loop kernel: [3][noct][nodes[1]][nf] (pass generation mod 3)
   Mailbox* mbox = nullptr;                 // loop kernel: rank-root mailbox (own allocation: IPC-exportable)
   double* rank_root = nullptr;  // [2][nf], double-buffered by pass parity
@@ -533,6 +539,64 @@ int build_graph(fcm_plan* p, double eps, int max_iters) {
 }  // namespace
 
 // ================================================================== C ABI ==
+// host-side row expansion for fcm_download_table (below)
+namespace {
+
+template <int C>
+void expand_u_c(const uint8_t* x, int64_t i0, int64_t i1, const double* tab, double* u) {
+  double* o = u + i0 * C;
+  int64_t i = i0;
+  if (C % 2 == 0) {
+    for (; i < i1; ++i) {
+      const double* t = tab + (int)x[i] * C;
+      for (int k = 0; k < C / 2; ++k) _mm_stream_pd(o + 2 * k, _mm_loadu_pd(t + 2 * k));
+      o += C;
+    }
+  } else {
+    for (; i + 2 <= i1; i += 2) {  // two rows = C aligned 16-byte stores
+      double r[2 * C];
+      const double* t0 = tab + (int)x[i] * C;
+      const double* t1 = tab + (int)x[i + 1] * C;
+      for (int k = 0; k < C; ++k) {
+        r[k] = t0[k];
+        r[C + k] = t1[k];
+      }
+      for (int k = 0; k < C; ++k) _mm_stream_pd(o + 2 * k, _mm_loadu_pd(r + 2 * k));
+      o += 2 * C;
+    }
+    for (; i < i1; ++i, o += C) std::memcpy(o, tab + (int)x[i] * C, sizeof(double) * C);
+  }
+}
+
+void expand_block(const uint8_t* x, int64_t i0, int64_t i1, int c, const double* tab, const int32_t* ltab,
+                  double* u, int32_t* lab) {
+  if (u) {
+    const bool aligned = (reinterpret_cast<uintptr_t>(u + i0 * c) & 15) == 0;
+    switch (aligned ? c : 0) {
+      case 2: expand_u_c<2>(x, i0, i1, tab, u); break;
+      case 3: expand_u_c<3>(x, i0, i1, tab, u); break;
+      case 4: expand_u_c<4>(x, i0, i1, tab, u); break;
+      case 5: expand_u_c<5>(x, i0, i1, tab, u); break;
+      case 6: expand_u_c<6>(x, i0, i1, tab, u); break;
+      case 7: expand_u_c<7>(x, i0, i1, tab, u); break;
+      case 8: expand_u_c<8>(x, i0, i1, tab, u); break;
+      default:
+        for (int64_t i = i0; i < i1; ++i) std::memcpy(u + i * c, tab + (int)x[i] * c, sizeof(double) * c);
+    }
+  }
+  if (lab) {
+    int64_t i = i0;
+    for (; i < i1 && (reinterpret_cast<uintptr_t>(lab + i) & 15); ++i) lab[i] = ltab[x[i]];
+    for (; i + 4 <= i1; i += 4)
+      _mm_stream_si128(reinterpret_cast<__m128i*>(lab + i),
+                       _mm_set_epi32(ltab[x[i + 3]], ltab[x[i + 2]], ltab[x[i + 1]], ltab[x[i]]));
+    for (; i < i1; ++i) lab[i] = ltab[x[i]];
+  }
+  _mm_sfence();
+}
+
+}  // namespace
+
 extern "C" {
 
 int fcm_abi_version(void) { return FCM_ABI_VERSION; }
@@ -997,6 +1061,96 @@ int fcm_download(fcm_plan* p, double* u_out, int32_t* labels_out) {
     if (labels_out)
       CK(cudaMemcpyAsync(labels_out + (s.g.voxel0 - host0), s.out_labels,
                          sizeof(int32_t) * s.g.n_local, cudaMemcpyDeviceToHost, s.stream));
+  }
+  for (int i = 0; i < p->nshards; ++i) {
+    CK(cudaSetDevice(p->sh[i].device));
+    CK(cudaStreamSynchronize(p->sh[i].stream));
+  }
+  return FCM_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Download by intensity table (uint8 pixels).  u_final and the labels are a
+// pure function of (x_i, v_final) -- the epilogue evaluates exactly that per
+// voxel -- so for 8-bit pixels the n x c result has at most 256 distinct
+// rows.  The epilogue runs once over the 256 intensities (same kernel, same
+// arithmetic: bit-identical rows), 256 x (8c + 4) bytes cross PCIe, and the
+// host expands the rows along its own copy of the pixels with streaming
+// stores on every core.  The device labels are still written (resident for
+// fcm_label_confusion / fcm_mask_overlap).
+
+int fcm_download_table(fcm_plan* p, const uint8_t* x_host, double* u_out, int32_t* labels_out,
+                       int32_t nthreads) {
+  if (check_plan(p)) return FCM_E_ARG;
+  if (!p->run_ok) return fail(p, FCM_E_STATE, "no successful fcm_run to download");
+  if (p->xkind != XK_U8) return fail(p, FCM_E_ARG, "fcm_download_table needs a uint8 plan");
+  if (!x_host && (u_out || labels_out)) return fail(p, FCM_E_ARG, "x_host is NULL");
+  // device labels stay resident (metrics); the 256-row table from shard 0
+  for (int i = 0; i < p->nshards; ++i) {
+    Shard& s = p->sh[i];
+    if (s.g.n_local == 0) continue;
+    CK(cudaSetDevice(s.device));
+    int rc;
+    if (!s.out_labels && (rc = dalloc(p, s, &s.out_labels, (size_t)s.g.n_local))) return rc;
+    EpilogueArgs e{};
+    e.x = s.x;
+    e.n = s.g.n_local;
+    e.c = p->c;
+    e.v = s.ctl->v;
+    e.m = p->pw.m;
+    e.p = p->pw.p;
+    e.pkind = p->pw.pkind;
+    e.pint = p->pw.pint;
+    e.mkind = p->pw.mkind;
+    e.mint = p->pw.mint;
+    e.u_out = nullptr;
+    e.labels = s.out_labels;
+    CK(launch_epilogue(p->xkind, p->c, p->mode, e, s.sms, s.stream));
+  }
+  Shard& s0 = p->sh[0];
+  CK(cudaSetDevice(s0.device));
+  int rc;
+  if (!s0.tab_x) {
+    if ((rc = dalloc(p, s0, &s0.tab_x, 256))) return rc;
+    if ((rc = dalloc(p, s0, &s0.tab_u, (size_t)256 * p->c))) return rc;
+    if ((rc = dalloc(p, s0, &s0.tab_l, 256))) return rc;
+    uint8_t ramp[256];
+    for (int b = 0; b < 256; ++b) ramp[b] = (uint8_t)b;
+    CK(cudaMemcpy(s0.tab_x, ramp, 256, cudaMemcpyHostToDevice));
+  }
+  EpilogueArgs e{};
+  e.x = s0.tab_x;
+  e.n = 256;
+  e.c = p->c;
+  e.v = s0.ctl->v;
+  e.m = p->pw.m;
+  e.p = p->pw.p;
+  e.pkind = p->pw.pkind;
+  e.pint = p->pw.pint;
+  e.mkind = p->pw.mkind;
+  e.mint = p->pw.mint;
+  e.u_out = s0.tab_u;
+  e.labels = s0.tab_l;
+  CK(launch_epilogue(p->xkind, p->c, p->mode, e, s0.sms, s0.stream));
+  std::vector<double> tab((size_t)256 * p->c);
+  int32_t ltab[256];
+  CK(cudaMemcpyAsync(tab.data(), s0.tab_u, sizeof(double) * tab.size(), cudaMemcpyDeviceToHost, s0.stream));
+  CK(cudaMemcpyAsync(ltab, s0.tab_l, sizeof(ltab), cudaMemcpyDeviceToHost, s0.stream));
+  CK(cudaStreamSynchronize(s0.stream));
+  // host expansion over the plan's voxel range (rank plans: the rank slice)
+  int64_t n = 0;
+  for (int i = 0; i < p->nshards; ++i) n += p->sh[i].g.n_local;
+  if (u_out || labels_out) {
+    int T = nthreads > 0 ? nthreads : (int)std::thread::hardware_concurrency();
+    T = (int)std::max<int64_t>(1, std::min<int64_t>(T, std::max<int64_t>(1, n >> 16)));
+    const int64_t chunk = ((n + T - 1) / T + 63) & ~int64_t(63);  // even starts keep the u rows 16-B aligned
+    std::vector<std::thread> th;
+    for (int t = 1; t < T; ++t) {
+      const int64_t i0 = t * chunk, i1 = std::min(n, i0 + chunk);
+      if (i0 < i1) th.emplace_back(expand_block, x_host, i0, i1, p->c, tab.data(), ltab, u_out, labels_out);
+    }
+    expand_block(x_host, 0, std::min(n, chunk), p->c, tab.data(), ltab, u_out, labels_out);
+    for (auto& t : th) t.join();
   }
   for (int i = 0; i < p->nshards; ++i) {
     CK(cudaSetDevice(p->sh[i].device));

@@ -195,6 +195,22 @@ class FcmPlan:
         check(lib().fcm_download(self._h, ptr(u), ptr(lab)), self._h, "fcm_download")
         return u, lab
 
+    def download_table(self, x: np.ndarray, membership: bool = True, labels: bool = True, u_out=None,
+                       labels_out=None, threads: int = 0):
+        """download() for uint8 plans through the 256-row intensity table: the same arrays bit for
+        bit, 256*(8c+4) bytes over PCIe, rows expanded on the host along `x` (the uploaded pixels)."""
+        x = np.ascontiguousarray(x, dtype=np.uint8)
+        if x.shape[0] != self.n_local:
+            raise DimensionMismatchError(f"pixels cover {x.shape[0]} voxels, expected {self.n_local}")
+        u = lab = None
+        if membership:
+            u = u_out if u_out is not None else np.empty(self.n_local * self.c, dtype=np.float64)
+        if labels:
+            lab = labels_out if labels_out is not None else np.empty(self.n_local, dtype=np.int32)
+        check(lib().fcm_download_table(self._h, ptr(x), ptr(u), ptr(lab), int(threads)), self._h,
+              "fcm_download_table")
+        return u, lab
+
     def profile(self) -> np.ndarray:
         """Loop-kernel timeline of the last run (FCM_OPT_PROFILE): array [pass, cta, slot]
         with slots 0 start, 1 claims done, 2 consumers done, 3 barrier released (ns), 4 tiles."""
@@ -302,7 +318,9 @@ def run_fcm_gpu(img: GrayImage, cfg: FcmConfig, devices=None,
         else:
             plan.upload_membership(initial_membership.u)
         v, trace, k, conv = plan.run(cfg.m, cfg.epsilon, cfg.max_iters)
-        u, labels = plan.download()
+        # 8-bit pixels: at most 256 distinct result rows -- copy the table,
+        # expand on the host (identical arrays, ~n*8c fewer PCIe bytes)
+        u, labels = plan.download_table(xx) if kind == _lib.FCM_X_U8 else plan.download()
     except BaseException:
         plan.close()
         raise

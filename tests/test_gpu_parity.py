@@ -356,3 +356,48 @@ def test_recompute_mode_matches_canonical(name, shards):
     assert ka == kb == r["iterations"] and ca == cb
     assert va.tobytes() == vb.tobytes() and ta.tobytes() == tb.tobytes()
     assert ua.tobytes() == ub.tobytes() and np.array_equal(la, lb)
+
+
+@pytest.mark.parametrize("n,c,m,shards,threads", [
+    (39_277, 3, 2.0, 1, 0), (1_000_003, 3, 2.0, 2, 0), (777, 2, 2.0, 1, 1), (250_001, 5, 1.5, 1, 3),
+    (131_073, 8, 1.5, 4, 0), (65_537, 7, 2.0, 1, 0), (100_000, 4, 3.0, 2, 2), (50_001, 16, 2.0, 1, 0)])
+def test_download_table_matches_download_bitwise(n, c, m, shards, threads):
+    """fcm_download_table (256-row intensity table, rows expanded on the host)
+    returns exactly fcm_download's arrays; the device labels it leaves behind
+    give the same label statistics."""
+    from paper_1601_00072_b200 import _lib
+    x = np.random.default_rng(n).integers(0, 256, n).astype(np.uint8)
+    with pkg.FcmPlan(n, c, _lib.FCM_X_U8, [0] * shards) as plan:
+        plan.upload_pixels(x)
+        plan.init_membership(7)
+        plan.run(m, 1e-5, 60)
+        u0, l0 = plan.download()
+        ref = (np.arange(n) % 3).astype(np.int32)
+        conf0 = plan.confusion(ref, 3)
+        u1, l1 = plan.download_table(x, threads=threads)
+        conf1 = plan.confusion(ref, 3)
+        # odd offsets: unaligned host buffers take the plain-store path
+        ub = np.empty(n * c + 1, dtype=np.float64)[1:]
+        lb = np.empty(n + 1, dtype=np.int32)[1:]
+        plan.download_table(x, u_out=ub, labels_out=lb)
+    assert u0.tobytes() == u1.tobytes() and np.array_equal(l0, l1)
+    assert u0.tobytes() == ub.tobytes() and np.array_equal(l0, lb)
+    assert np.array_equal(conf0, conf1)
+
+
+def test_run_fcm_gpu_uint8_uses_table_download():
+    """run_fcm_gpu on 8-bit pixels returns the same FcmResult arrays as the
+    per-voxel download (the table path is the default for uint8)."""
+    from paper_1601_00072_b200 import _lib
+    r = run_case("C1")
+    x = r["x"].astype(np.uint8)
+    res = pkg.run_fcm_gpu(pkg.GrayImage(width=x.shape[0], height=1, pixels=x.astype(np.float64)),
+                          pkg.FcmConfig(c=r["c"], m=r["m"], epsilon=r["epsilon"], max_iters=r["max_iters"],
+                                        seed=r["seed"]))
+    with pkg.FcmPlan(x.shape[0], r["c"], _lib.FCM_X_U8) as plan:
+        plan.upload_pixels(x)
+        plan.init_membership(r["seed"])
+        plan.run(r["m"], r["epsilon"], r["max_iters"])
+        u, lab = plan.download()
+    assert np.asarray(res.membership.u).tobytes() == u.tobytes()
+    assert np.array_equal(np.asarray(res.labels.labels).reshape(-1), lab)
