@@ -115,6 +115,12 @@ class ClockSampler:
             self.lines.append(line.strip())
 
     def __exit__(self, *exc):
+        self.post = False
+        if self.proc and not self.lines:  # region shorter than the 50 ms period: take the next sample
+            t0 = time.time()
+            while not self.lines and time.time() - t0 < 0.5:
+                time.sleep(0.005)
+            self.post = bool(self.lines)
         if self.proc:
             self.proc.terminate()
             try:
@@ -143,8 +149,11 @@ class ClockSampler:
                 pass
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(smax), "reasons": sorted(reasons),
-                "samples": len(sm), "power_w": statistics.median(pw) if pw else None}
+        out = {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(smax), "reasons": sorted(reasons),
+               "samples": len(sm), "power_w": statistics.median(pw) if pw else None}
+        if getattr(self, "post", False):
+            out["note"] = "timed region shorter than the 50 ms sampling period: first sample right after it"
+        return out
 
 
 def make_volume(shape, rank_slice=None):
