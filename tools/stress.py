@@ -51,5 +51,12 @@ while time.time() < t_end:
                 print("NONDETERMINISTIC", n, c, m, shards, flush=True)
                 sys.exit(1)
             solves += 1
+        if first not in (None, "dead") and n <= 1_000_003 and rng.random() < 0.5:
+            # table download == per-voxel download, bit for bit
+            u0, l0 = plan.download()
+            u1, l1 = plan.download_table(x, threads=int(rng.integers(0, 5)))
+            if u0.tobytes() != u1.tobytes() or not np.array_equal(l0, l1):
+                print("TABLE DOWNLOAD MISMATCH", n, c, m, shards, flush=True)
+                sys.exit(3)
     cases += 1
 print(f"stress ok: {cases} cases, {solves} solves", flush=True)
