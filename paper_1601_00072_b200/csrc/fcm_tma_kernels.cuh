@@ -95,9 +95,11 @@ __global__ void __launch_bounds__(kTmaThreads, 2) loop_tma_kernel(PassArgs a) {
   __shared__ double sdelta;       // recompute mode: delta of this pass from the tables
   __shared__ uint32_t spresent[8];
   __shared__ int s_done;
+  __shared__ __align__(8) uint64_t upbar;  // bulk copy of the tile partials (small volumes)
   const int tid = threadIdx.x;
   const int c = C <= 8 ? C : a.c;
   if (tid == 0) {
+    mbar_init(smem_u32(&upbar), 1);
     tma_init_barriers<XT, C, MODE>(smem, rs);
     s_done = *(volatile int*)&a.ctl->done;
     for (int j = 0; j < c; ++j) vsh[j] = __ldcg(&a.ctl->v[j]);
@@ -118,6 +120,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) loop_tma_kernel(PassArgs a) {
   unsigned gen = 0;  // grid-barrier generations
   // monotone tile scheduler: every producer makes exactly one failing claim
   // per pass, so pass p hands out [p(T+G), p(T+G)+T) -- no per-pass reset
+  uint32_t upphase = 0;
   unsigned sched = 0;
   const unsigned sched_step = (unsigned)a.g.tiles_local + gridDim.x;
   __syncthreads();
@@ -182,7 +185,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) loop_tma_kernel(PassArgs a) {
     __syncthreads();
     if (s_done) break;
     loop_upper<NF>(a, l1, reinterpret_cast<double*>(smem), oroot, rs.root, it, from_tiles,
-                   (recomp && it >= 2) ? sdelta : 0.0);
+                   (recomp && it >= 2) ? sdelta : 0.0, smem_u32(&upbar), &upphase, L::kRingBytes / 8);
     if (tid == 0) probe(a, it, 10, global_ns());
     if (a.mb_ranks > 1 && !exchange_roots(a, rs.root, gen)) {
       if (tid == 0) {

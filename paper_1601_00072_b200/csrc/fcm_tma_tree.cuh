@@ -253,7 +253,9 @@ __device__ __forceinline__ double tree32(const double* p, int64_t stride, int nr
 template <int NF>
 __device__ __forceinline__ void loop_upper(const PassArgs& a, const double* l1, double* scratch,
                                            double (*oroot)[NF], double* root, unsigned it = 0,
-                                           bool from_tiles = false, double extra_delta = 0.0) {
+                                           bool from_tiles = false, double extra_delta = 0.0,
+                                           uint32_t upbar = 0u, uint32_t* upphase = nullptr,
+                                           int64_t scratch_doubles = 0) {
   const int tid = threadIdx.x;
   const int nf = 2 * a.c + 2;
   const Geometry& g = a.g;
@@ -264,13 +266,31 @@ __device__ __forceinline__ void loop_upper(const PassArgs& a, const double* l1, 
   if (from_tiles) {
     double* l1s = scratch;
     scratch += (int64_t)g.noct * g.nodes[1] * NF;
+    // the rank's tile partials in one bulk copy (TMA) into the idle ring when
+    // they fit: one request stream per CTA instead of 32 dependent loads per
+    // thread against the same hot L2 lines
+    double* tcopy = scratch + kOctants * NF;  // after the upper scratch (levels <= 2 here)
+    const int64_t tdoubles = (int64_t)g.tiles_local * nf;
+    const bool bulk = upbar != 0u && tdoubles > 0 && (tcopy - l1s) + tdoubles <= scratch_doubles;
+    if (bulk) {
+      if (tid == 0) {
+        fence_proxy_async_global();  // partials: generic stores published by the grid barrier
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive_tx(upbar, (uint32_t)(tdoubles * 8));
+        bulk_g2s(smem_u32(tcopy), a.tile_part, (uint32_t)(tdoubles * 8), upbar);
+      }
+      mbar_wait(upbar, *upphase);
+      *upphase ^= 1u;
+    }
     for (int pr = tid; pr < g.noct * g.nodes[1] * nf; pr += kTmaThreads) {
       const int z = pr / nf, f = pr - z * nf;
       const int lo = z / g.nodes[1], j = z - lo * g.nodes[1];
       const int oct = g.oct0 + lo;
       const int nreal = (int64_t)oct * g.M < g.T ? node_real_children(g, oct, 1, j) : 0;
-      const double* src = a.tile_part + ((int64_t)oct * g.M - g.tile0 + (int64_t)j * kFan) * nf + f;
-      l1s[(int64_t)z * NF + f] = nreal ? tree32<true>(src, nf, nreal, f == nf - 1) : 0.0;
+      const int64_t off = ((int64_t)oct * g.M - g.tile0 + (int64_t)j * kFan) * nf + f;
+      l1s[(int64_t)z * NF + f] = nreal == 0 ? 0.0
+                                 : bulk   ? tree32<false>(tcopy + off, nf, nreal, f == nf - 1)
+                                          : tree32<true>(a.tile_part + off, nf, nreal, f == nf - 1);
     }
     __syncthreads();
     if (tid == 0) probe(a, it, 17, global_ns());
