@@ -68,10 +68,17 @@ typedef enum {
   FCM_OPT_PROFILE = 8, /* 1: the loop kernel records a per-CTA timeline (fcm_last_profile) */
   FCM_OPT_SEED_PASS = 9, /* 1 (default): with a seeded start the loop kernel generates u_0 as its
                            pass 0; 0: a separate prologue kernel does */
-  FCM_OPT_RECOMPUTE = 11 /* 1: "effective" mode (uint8 pixels, m == 2, seeded start, loop kernel):
+  FCM_OPT_RECOMPUTE = 11, /* 1: "effective" mode (uint8 pixels, m == 2, seeded start, loop kernel):
                            passes >= 2 read x only and write u_k; delta_k is taken between the fp64
                            intensity tables of passes k-1 and k over the intensities present
                            (u_{k-1} is recomputed from (x, v_{k-1}), never read back).  0: default */
+  FCM_OPT_DEBUG_DELAY = 12, /* diagnostics: after every grid barrier of the loop kernel one CTA (a
+                              different one each pass) sleeps this many ns (<= 10 ms) before it reads
+                              the pass's partials -- results must not change (race test).  0: default */
+  FCM_OPT_DEBUG_SHARED_PARTIALS = 13 /* diagnostics: 1 = every pass of the loop kernel's small-volume
+                              path publishes its tile partials into the same buffer (the round-1
+                              layout, racy under FCM_OPT_DEBUG_DELAY; shows the race test can fail).
+                              0: default (two buffers alternated by pass parity) */
 } fcm_option;
 
 typedef struct fcm_plan fcm_plan;

@@ -122,6 +122,8 @@ struct fcm_plan {
   int profile = 0;  // record the loop kernel's per-CTA timeline
   int seed_pass = 1;  // loop kernel generates the seeded u_0 as its pass 0
   int recompute = 0;  // loop kernel: "effective" mode, passes >= 2 stream x only
+  unsigned debug_delay_ns = 0;  // loop kernel: one CTA per pass sleeps after the grid barrier (tests)
+  int debug_shared_parts = 0;   // loop kernel: single tile-partial buffer (the racy round-1 layout; tests)
   unsigned run_counter = 0;  // fcm_run calls (mailbox tags); identical on every rank
   bool p2p_ready = false;    // multi-process ranks: peer mailboxes mapped (fcm_connect_peers)
   Mailbox* peer_mbox[kOctants] = {};
@@ -252,7 +254,7 @@ int setup_shard(fcm_plan* p, Shard& s) {
   if ((rc = dalloc(p, s, &s.u, (size_t)s.g.plane * p->c))) return rc;
   const double resident = (double)s.g.plane * (double)(xsz + 4 * p->c);
   s.keep_l2 = resident <= 0.8 * (double)prop.l2CacheSize ? 1 : 0;
-  if ((rc = dalloc(p, s, &s.tile_part, (size_t)std::max(s.g.tiles_local, 1) * nf))) return rc;
+  if ((rc = dalloc(p, s, &s.tile_part, (size_t)2 * std::max(s.g.tiles_local, 1) * nf))) return rc;
   size_t cnt_total = 0;
   for (int l = 1; l <= s.g.levels; ++l) {
     if ((rc = dalloc(p, s, &s.node_part[l], (size_t)s.g.noct * s.g.nodes[l] * nf))) return rc;
@@ -274,7 +276,7 @@ int setup_shard(fcm_plan* p, Shard& s) {
   CK(cudaMemsetAsync(s.node_cnt[1], 0, sizeof(unsigned) * s.cnt_total, s.stream));
   CK(cudaMemsetAsync(s.ctl, 0, sizeof(Control), s.stream));
   // every tree slot starts unpublished (all-ones NaN pattern, see fcm_kernels.cuh)
-  CK(cudaMemsetAsync(s.tile_part, 0xff, sizeof(double) * std::max(s.g.tiles_local, 1) * nf, s.stream));
+  CK(cudaMemsetAsync(s.tile_part, 0xff, sizeof(double) * 2 * std::max(s.g.tiles_local, 1) * nf, s.stream));
   for (int l = 1; l <= s.g.levels; ++l)
     CK(cudaMemsetAsync(s.node_part[l], 0xff, sizeof(double) * s.g.noct * s.g.nodes[l] * nf, s.stream));
   return FCM_OK;
@@ -755,6 +757,11 @@ int fcm_set_option(fcm_plan* p, int32_t key, int64_t value) {
     case FCM_OPT_PROFILE: p->profile = value ? 1 : 0; return FCM_OK;
     case FCM_OPT_SEED_PASS: p->seed_pass = value ? 1 : 0; return FCM_OK;
     case FCM_OPT_RECOMPUTE: p->recompute = value ? 1 : 0; return FCM_OK;
+    case FCM_OPT_DEBUG_DELAY:
+      if (value < 0 || value > 10000000) return FCM_E_ARG;  // <= 10 ms
+      p->debug_delay_ns = (unsigned)value;
+      return FCM_OK;
+    case FCM_OPT_DEBUG_SHARED_PARTIALS: p->debug_shared_parts = value ? 1 : 0; return FCM_OK;
     case FCM_OPT_L2:
       if (value < 0 || value > 2) return FCM_E_ARG;
       p->l2_mode = (int)value;
@@ -859,7 +866,7 @@ int fcm_run(fcm_plan* p, double m, double eps, int32_t max_iters, double* v_out,
     CK(cudaMemcpyAsync(s.ctl, p->host_tmpl, sizeof(Control), cudaMemcpyHostToDevice, s.stream));
     CK(cudaMemsetAsync(s.node_cnt[1], 0, sizeof(unsigned) * s.cnt_total, s.stream));
     const int nf = nf_of(p->c);
-    CK(cudaMemsetAsync(s.tile_part, 0xff, sizeof(double) * std::max(s.g.tiles_local, 1) * nf, s.stream));
+    CK(cudaMemsetAsync(s.tile_part, 0xff, sizeof(double) * 2 * std::max(s.g.tiles_local, 1) * nf, s.stream));
     for (int l = 1; l <= s.g.levels; ++l)
       CK(cudaMemsetAsync(s.node_part[l], 0xff, sizeof(double) * s.g.noct * s.g.nodes[l] * nf, s.stream));
     CK(cudaMemsetAsync(s.l1_buf, 0xff, sizeof(double) * 3 * s.g.noct * s.g.nodes[1] * nf, s.stream));
@@ -906,6 +913,8 @@ int fcm_run(fcm_plan* p, double m, double eps, int32_t max_iters, double* v_out,
       a.mbox_local = s.mbox;
       for (int r = 0; r < p->nranks; ++r) a.mbox_peer[r] = p->nshards > 1 ? p->sh[r].mbox : p->peer_mbox[r];
       a.finalize_local = 1;  // every rank finalizes from the exchanged global root
+      a.debug_delay_ns = p->debug_delay_ns;
+      a.debug_shared_parts = p->debug_shared_parts;
       if (p->profile && i == 0) {
         const int passes = std::min(max_iters, 64);
         if (!p->prof) {

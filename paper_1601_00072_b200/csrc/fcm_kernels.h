@@ -23,7 +23,8 @@ struct PassArgs {
   int max_iters;
   int seq;                // pass sequence number in this run (tile-scheduler parity)
   Geometry g;
-  double* tile_part;      // level 0: [tiles_local][nf]
+  double* tile_part;      // level 0: [2][tiles_local][nf] (the loop kernel's small-volume path
+                          // alternates the two halves by pass parity; every other path uses half 0)
   double* node_part[kMaxLevels + 1];  // level l >= 1: [noct][nodes[l]][nf]
   unsigned* node_cnt[kMaxLevels + 1]; // level l >= 1: [noct][nodes[l]] arrival counters
   double* rank_root;      // [nf]
@@ -43,6 +44,9 @@ struct PassArgs {
   Mailbox* mbox_peer[kOctants];     // every rank's mailbox as mapped here (peer / IPC pointers)
   uint64_t* prof;         // loop-kernel timeline [prof_passes][grid][kProbeSlots] or null
   int prof_passes;
+  unsigned debug_delay_ns;  // FCM_OPT_DEBUG_DELAY: one CTA per pass sleeps this long after the grid
+                            // barrier (race-detection test; 0 in production)
+  int debug_shared_parts;   // FCM_OPT_DEBUG_SHARED_PARTIALS: one tile-partial buffer for every pass
 };
 constexpr int kProbeSlots = 20;
 

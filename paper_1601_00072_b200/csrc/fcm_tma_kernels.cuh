@@ -131,6 +131,13 @@ __global__ void __launch_bounds__(kTmaThreads, 2) loop_tma_kernel(PassArgs a) {
     // ctl->l1_done (fence + atomic per node); readers wait for the count
     const unsigned gnext = gen + 1;
     double* l1 = a.l1_buf + (gnext % 3) * l1_len;
+    // small volumes: this pass's tile partials go to the half of tile_part of
+    // its parity.  Every CTA reads them after the grid barrier while early
+    // CTAs may already publish the next pass's partials -- into the other
+    // half; pass it+2 reuses this half only after the barrier of pass it+1,
+    // which no CTA passes before every CTA has finished reading.
+    double* tpart = a.tile_part + (from_tiles && !a.debug_shared_parts
+                                   ? (int64_t)(gnext & 1u) * a.g.tiles_local * (2 * a.c + 2) : 0);
     if (tid >= kThreads) {
       if (tid == kProducerTid) {
         fence_proxy_async_global();
@@ -145,7 +152,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) loop_tma_kernel(PassArgs a) {
       if ((tid >> 5) == kReducerWarp) {
         // slots first (then arrive at the pass-end barrier), owned level-1
         // nodes after -- overlapping the grid barrier
-        tma_reduce<C, true>(a, rs, sp, &a.ctl->tile_next[1], l1, it, from_tiles, sched);
+        tma_reduce<C, true>(a, rs, sp, &a.ctl->tile_next[1], l1, it, from_tiles, sched, tpart);
         if ((tid & 31) == 0) probe(a, it, 7, global_ns());
       } else {
         bar_sync_end();
@@ -184,8 +191,15 @@ __global__ void __launch_bounds__(kTmaThreads, 2) loop_tma_kernel(PassArgs a) {
     }
     __syncthreads();
     if (s_done) break;
+    if (a.debug_delay_ns) {  // race test: one CTA (a different one each pass) reads late
+      if (tid == 0 && blockIdx.x == (it * 7u + 1u) % gridDim.x) {
+        const uint64_t t0 = global_ns();
+        while (global_ns() - t0 < a.debug_delay_ns) __nanosleep(1000);
+      }
+      __syncthreads();
+    }
     loop_upper<NF>(a, l1, reinterpret_cast<double*>(smem), oroot, rs.root, it, from_tiles,
-                   (recomp && it >= 2) ? sdelta : 0.0, smem_u32(&upbar), &upphase, L::kRingBytes / 8);
+                   (recomp && it >= 2) ? sdelta : 0.0, smem_u32(&upbar), &upphase, L::kRingBytes / 8, tpart);
     if (tid == 0) probe(a, it, 10, global_ns());
     if (a.mb_ranks > 1 && !exchange_roots(a, rs.root, gen)) {
       if (tid == 0) {

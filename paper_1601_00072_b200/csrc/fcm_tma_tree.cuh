@@ -106,7 +106,8 @@ __device__ __forceinline__ void upper_node(const Geometry& g, int k, int& l, int
 template <int C, bool LOOP>
 __device__ __forceinline__ void tma_reduce(const PassArgs& a, RedSlots<2 * C + 2>& rs, Pipe& sp,
                                            const unsigned* counter, double* l1_out, unsigned it = 0,
-                                           bool no_owners = false, unsigned base = 0) {
+                                           bool no_owners = false, unsigned base = 0,
+                                           double* tile_out = nullptr) {
   constexpr int NF = 2 * C + 2;
   const int lane = threadIdx.x & 31;
   const int nf = 2 * a.c + 2;
@@ -114,6 +115,9 @@ __device__ __forceinline__ void tma_reduce(const PassArgs& a, RedSlots<2 * C + 2
   const int G = gridDim.x;
   const bool cta0 = blockIdx.x == 0;
   const int NA = no_owners ? 0 : g.noct * g.nodes[1];  // list A: level-1 nodes
+  // tile partials go to half 0 of tile_part, or (loop kernel, small volumes)
+  // to the half of this pass's parity
+  double* const tpart = tile_out ? tile_out : a.tile_part;
   int per = 0;
   for (int m = 2; m <= g.levels; ++m) per += g.nodes[m];
   const int NB = (!LOOP && cta0) ? g.noct * per : 0;  // list B: CTA 0's upper levels
@@ -148,7 +152,7 @@ __device__ __forceinline__ void tma_reduce(const PassArgs& a, RedSlots<2 * C + 2
           const double q1 = combine(w[2][f], w[3][f], mx);
           const double q2 = combine(w[4][f], w[5][f], mx);
           const double q3 = combine(w[6][f], w[7][f], mx);
-          st_relaxed(a.tile_part + (int64_t)t * nf + f, combine(combine(q0, q1, mx), combine(q2, q3, mx), mx));
+          st_relaxed(tpart + (int64_t)t * nf + f, combine(combine(q0, q1, mx), combine(q2, q3, mx), mx));
         }
       } else {
         slots_done = true;
@@ -255,7 +259,7 @@ __device__ __forceinline__ void loop_upper(const PassArgs& a, const double* l1, 
                                            double (*oroot)[NF], double* root, unsigned it = 0,
                                            bool from_tiles = false, double extra_delta = 0.0,
                                            uint32_t upbar = 0u, uint32_t* upphase = nullptr,
-                                           int64_t scratch_doubles = 0) {
+                                           int64_t scratch_doubles = 0, const double* tparts = nullptr) {
   const int tid = threadIdx.x;
   const int nf = 2 * a.c + 2;
   const Geometry& g = a.g;
@@ -264,6 +268,7 @@ __device__ __forceinline__ void loop_upper(const PassArgs& a, const double* l1, 
   // from the tile partials the grid barrier published, into shared memory
   if (tid == 0) probe(a, it, 16, global_ns());
   if (from_tiles) {
+    const double* tp = tparts ? tparts : a.tile_part;  // this pass's half of the tile partials
     double* l1s = scratch;
     scratch += (int64_t)g.noct * g.nodes[1] * NF;
     // the rank's tile partials in one bulk copy (TMA) into the idle ring when
@@ -277,7 +282,7 @@ __device__ __forceinline__ void loop_upper(const PassArgs& a, const double* l1, 
         fence_proxy_async_global();  // partials: generic stores published by the grid barrier
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_arrive_tx(upbar, (uint32_t)(tdoubles * 8));
-        bulk_g2s(smem_u32(tcopy), a.tile_part, (uint32_t)(tdoubles * 8), upbar);
+        bulk_g2s(smem_u32(tcopy), tp, (uint32_t)(tdoubles * 8), upbar);
       }
       mbar_wait(upbar, *upphase);
       *upphase ^= 1u;
@@ -290,7 +295,7 @@ __device__ __forceinline__ void loop_upper(const PassArgs& a, const double* l1, 
       const int64_t off = ((int64_t)oct * g.M - g.tile0 + (int64_t)j * kFan) * nf + f;
       l1s[(int64_t)z * NF + f] = nreal == 0 ? 0.0
                                  : bulk   ? tree32<false>(tcopy + off, nf, nreal, f == nf - 1)
-                                          : tree32<true>(a.tile_part + off, nf, nreal, f == nf - 1);
+                                          : tree32<true>(tp + off, nf, nreal, f == nf - 1);
     }
     __syncthreads();
     if (tid == 0) probe(a, it, 17, global_ns());

@@ -401,3 +401,48 @@ def test_run_fcm_gpu_uint8_uses_table_download():
         u, lab = plan.download()
     assert np.asarray(res.membership.u).tobytes() == u.tobytes()
     assert np.array_equal(np.asarray(res.labels.labels).reshape(-1), lab)
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3@200000"])
+def test_late_cta_after_grid_barrier_bitwise(name):
+    """Race test for the loop kernel's small-volume path (<= 1024 tiles: every
+    CTA reduces the tile partials itself after the grid barrier).  One CTA per
+    pass (a different one each pass) sleeps 100 us between the barrier and its
+    reads while the others run ahead into the next pass and publish new tile
+    partials.  The partials alternate between two buffers by pass parity, so
+    the late reader still sees its own pass: every result is bit-identical to
+    the undelayed run (the reference's determinism contract,
+    parallel.py:1-11, test_parallel.py:214-264)."""
+    from paper_1601_00072_b200 import _lib
+    from paper_1601_00072_b200.phantom import make_config
+    x = make_config(name).reshape(-1).astype(np.uint8)
+
+    def solve(delay_ns, shared=0):
+        with pkg.FcmPlan(x.shape[0], 3, _lib.FCM_X_U8) as plan:
+            plan.upload_pixels(x)
+            plan.init_membership(0)
+            plan.set_option(_lib.FCM_OPT_DEBUG_DELAY, delay_ns)
+            plan.set_option(_lib.FCM_OPT_DEBUG_SHARED_PARTIALS, shared)
+            v, trace, k, conv = plan.run(2.0, 1e-5, 500)
+            t = plan.timing()
+            u, lab = plan.download()
+            assert plan.info()["tiles_local"] <= 1024
+        return v, trace, k, conv, u, lab, t
+
+    base = solve(0)
+    late = solve(100_000)
+    assert late[6]["passes_launched"] == 1  # the loop kernel ran the solve
+    # the injected sleeps really happened: >= 100 us per pass
+    assert late[6]["loop_ms"] - base[6]["loop_ms"] >= 0.1 * base[2] * 0.9
+    assert late[2] == base[2] and late[3] == base[3]
+    assert late[0].tobytes() == base[0].tobytes() and late[1].tobytes() == base[1].tobytes()
+    assert late[4].tobytes() == base[4].tobytes() and np.array_equal(late[5], base[5])
+    # negative control: the round-1 layout (one partial buffer for every pass)
+    # under the same delay is corrupted -- CTAs disagree on v / the stop test
+    # and the grid barrier times out (tools/race_probe.py, profiles/race_probe_r02.txt)
+    try:
+        racy = solve(100_000, shared=1)
+    except pkg.FcmError:
+        racy = None
+    assert racy is None or racy[2] != base[2] or racy[0].tobytes() != base[0].tobytes() \
+        or racy[1].tobytes() != base[1].tobytes() or racy[4].tobytes() != base[4].tobytes()
