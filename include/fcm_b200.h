@@ -46,6 +46,7 @@ typedef enum {
 
 typedef enum {
   FCM_X_U8 = 0,  /* integer intensities 0..255 (every BASELINE config): 1 byte per voxel in HBM */
+  FCM_X_U16 = 1, /* integer intensities 0..65535 (16-bit PGM rasters, imgio.py:102-110): 2 bytes per voxel */
   FCM_X_F64 = 2  /* any finite, non-negative intensity (types.py:38-41) */
 } fcm_x_kind;
 
@@ -91,7 +92,7 @@ int fcm_device_count(int32_t* count);
  * Engine loop (replaces core._iterate / parallel._iterate)
  * ---------------------------------------------------------------------- */
 
-/* Single-process plan over n voxels and c clusters (2 <= c <= 16), sharded
+/* Single-process plan over n voxels and c clusters (2 <= c <= 32), sharded
  * over nshards in {1,2,4,8} shards placed on devices[0..nshards-1] (a device
  * may repeat: shards on one GPU exercise the multi-GPU reduction exactly).
  * Mirrors run_fcm_parallel's workers= (parallel.py:334-362): results are
@@ -192,11 +193,32 @@ int fcm_mask_overlap(fcm_plan* plan, const uint8_t* mask, int64_t* counts_out);
  * ran the seeded start as its pass 0. */
 int fcm_last_timing(const fcm_plan* plan, double* out, int32_t count);
 
+/* delta_1..delta_k of the last fcm_run (out[0..min(count, iterations))):
+ * max |u_k - u_{k-1}| per pass, as the stop test compared it with epsilon
+ * (core.py:128-130).  Taken in fp64 against the fp32-stored u_{k-1} (within
+ * 3e-8 of the reference's fp64 delta) and rounded UP to 20 mantissa bits, so
+ * the stop test never fires early; parity tests log |delta - epsilon| of the
+ * last two passes against that error. */
+int fcm_delta_trace(const fcm_plan* plan, double* out, int32_t count);
+
 /* Loop-kernel timeline of the last fcm_run with FCM_OPT_PROFILE (diagnostics):
  * out[(pass * grid + cta) * 16 + k], k = 0 pass start, 1 producer done claiming,
  * 2 consumers done, 3 grid barrier released (globaltimer ns), 4 tiles claimed.
  * count must be >= passes * grid * 16; passes <= min(max_iters, 64). */
 int fcm_last_profile(const fcm_plan* plan, uint64_t* out, int64_t count, int32_t* passes, int32_t* grid);
+
+/* The 256-row result table of the last fcm_download_table: u_tab[b*c + j] is
+ * the fp64 membership row and l_tab[b] the label of intensity b.  Every row
+ * of the expanded result is a copy of one of these, so validating the table
+ * validates the result (types.py:82-85) without a pass over n*c doubles. */
+int fcm_result_table(const fcm_plan* plan, double* u_tab, int32_t* l_tab);
+
+/* Host-only: float64 intensities -> x_kind (FCM_X_U8: every value an integer
+ * in 0..255; FCM_X_U16: in 0..65535) on nthreads threads (<= 0: all cores),
+ * check and conversion in one pass.  FCM_E_ARG (out unspecified) when any
+ * value does not convert exactly.  The drop-in uses it to pick the narrowest
+ * exact device representation of GrayImage.pixels (types.py:38-41). */
+int fcm_narrow_pixels(const double* x, int64_t n, int32_t x_kind, void* out, int32_t nthreads);
 
 /* Page-lock caller memory so uploads/downloads run at full PCIe speed. */
 int fcm_host_register(void* ptr, int64_t bytes);

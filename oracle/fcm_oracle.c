@@ -226,6 +226,13 @@ void oracle_argmax_rows(const double *u, int32_t *labels_out, int64_t n, int64_t
  * Returns 0, or 1 + dead cluster index when update_centers reports a dead
  * cluster (the reference raises DegenerateClusterError there, core.py:122-123).
  */
+/* delta_{k-1} and delta_k of the last two iterations of the last iterate
+ * call (the values the stop test compared with epsilon, core.py:128-130):
+ * parity tests log their margins |delta - epsilon|.
+ * Not thread-safe; test infrastructure only. */
+static double g_deltas[2] = {0.0, 0.0};
+void oracle_last_deltas(double *out) { out[0] = g_deltas[0]; out[1] = g_deltas[1]; }
+
 int64_t oracle_iterate_sequential(const double *x, double *u, int64_t n, int64_t c, double m,
                                   double epsilon, int64_t max_iters, double *v_out,
                                   double *trace, int64_t *iterations, int32_t *converged) {
@@ -240,6 +247,7 @@ int64_t oracle_iterate_sequential(const double *x, double *u, int64_t n, int64_t
         if (dead >= 0) { status = 1 + dead; break; }
         oracle_update_membership_range(x, v_out, nxt, c, m, 0, n);
         double delta = oracle_max_abs_diff(cur, nxt, 0, n * c);
+        g_deltas[0] = g_deltas[1]; g_deltas[1] = delta;
         trace[it] = oracle_objective_linear(x, nxt, v_out, n, c, m);
         double *t = cur; cur = nxt; nxt = t;
         *iterations += 1;
@@ -309,6 +317,7 @@ int64_t oracle_iterate_parallel(const double *x, double *u, int64_t n, int64_t c
         PAR_RANGES(nblocks, oracle_block_reduce_range(terms, partials, n, block_size, lo, hi))
         trace[it] = oracle_linear_sum(partials, nblocks);
         double delta = oracle_max_abs_diff(cur, nxt, 0, n * c);
+        g_deltas[0] = g_deltas[1]; g_deltas[1] = delta;
         double *t = cur; cur = nxt; nxt = t;
         *iterations += 1;
         if (delta < epsilon) { *converged = 1; break; }

@@ -71,6 +71,7 @@ def lib():
         L.oracle_iterate_parallel.argtypes = it_args + [
             _i64, _dp, _dp, ctypes.POINTER(_i64), ctypes.POINTER(ctypes.c_int32)]
         L.oracle_iterate_parallel.restype = _i64
+        L.oracle_last_deltas.argtypes = [_dp]
         _lib = L
     return _lib
 
@@ -165,6 +166,14 @@ def argmax_rows(u, c: int) -> np.ndarray:
     labels = np.empty(n, dtype=np.int32)
     lib().oracle_argmax_rows(_p(u), labels.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), n, c)
     return labels
+
+
+def last_deltas() -> np.ndarray:
+    """(delta_{k-1}, delta_k) of the last two iterations of the last
+    iterate()/run_fcm() call (max |u_k - u_{k-1}|, core.py:128-130)."""
+    out = np.zeros(2)
+    lib().oracle_last_deltas(_p(out))
+    return out
 
 
 def iterate(x, u0, c: int, m: float, epsilon: float, max_iters: int, engine="sequential",

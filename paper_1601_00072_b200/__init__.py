@@ -22,6 +22,7 @@ from .engine import (
     membership_delta,
     objective,
     pixel_kind,
+    release_cached_plans,
     run_fcm_gpu,
     update_centers,
     update_membership,
@@ -37,7 +38,7 @@ __version__ = "0.1.0"
 
 __all__ = [
     "C_MAX", "ENGINES", "FcmPlan", "_iterate", "defuzzify", "init_membership", "membership_delta",
-    "objective", "pixel_kind", "run_fcm_gpu", "update_centers", "update_membership",
+    "objective", "pixel_kind", "release_cached_plans", "run_fcm_gpu", "update_centers", "update_membership",
     "DegenerateClusterError", "DeviceError", "DimensionMismatchError", "FcmError", "InvalidConfigError",
     "ROW_SUM_TOL", "ClusterCenters", "FcmConfig", "FcmResult", "GrayImage", "LabelMap", "MembershipMatrix",
     "MalformedHeaderError", "MissingClassError", "PgmError", "PgmValueError", "TruncatedRasterError",

@@ -15,7 +15,7 @@ from .errors import DegenerateClusterError, DeviceError, FcmError, InvalidConfig
 LIB_PATH = os.environ.get("FCM_B200_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libfcm_b200.so")
 
 FCM_OK, FCM_E_ARG, FCM_E_CUDA, FCM_E_NCCL, FCM_E_DEGENERATE, FCM_E_STATE, FCM_E_NOMEM = range(7)
-FCM_X_U8, FCM_X_F64 = 0, 2
+FCM_X_U8, FCM_X_U16, FCM_X_F64 = 0, 1, 2
 FCM_OPT_BATCH, FCM_OPT_TIMING, FCM_OPT_GRID, FCM_OPT_KERNEL, FCM_OPT_GRAPH = 1, 2, 3, 4, 5
 FCM_OPT_LOOP, FCM_OPT_L2, FCM_OPT_PROFILE, FCM_OPT_SEED_PASS = 6, 7, 8, 9
 FCM_OPT_RECOMPUTE, FCM_OPT_DEBUG_DELAY, FCM_OPT_DEBUG_SHARED_PARTIALS = 11, 12, 13
@@ -50,6 +50,10 @@ SIGNATURES = {
     "fcm_download_table": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32],
                            ctypes.c_int),
     "fcm_last_timing": ([ctypes.c_void_p, ctypes.POINTER(ctypes.c_double), ctypes.c_int32], ctypes.c_int),
+    "fcm_delta_trace": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32], ctypes.c_int),
+    "fcm_result_table": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
+    "fcm_narrow_pixels": ([ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p, ctypes.c_int32],
+                          ctypes.c_int),
     "fcm_last_profile": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.POINTER(ctypes.c_int32),
                           ctypes.POINTER(ctypes.c_int32)], ctypes.c_int),
     "fcm_host_register": ([ctypes.c_void_p, ctypes.c_int64], ctypes.c_int),

@@ -12,6 +12,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <limits>
 #include <string>
 #include <thread>
 #include <vector>
@@ -25,6 +26,30 @@
 #include "fcm_ops.h"
 
 using namespace fcm;
+
+static size_t xkind_bytes(int xkind) {  // bytes per voxel of x in HBM
+  return xkind == XK_U8 ? 1 : (xkind == XK_U16 ? 2 : 8);
+}
+
+// Host-only: float64 intensities -> the narrowest exact plan kind.  Every
+// value must be an integer in range (NaN, negatives and fractions fail);
+// the check and the conversion are one pass on `nthreads` threads.
+namespace {
+template <typename T>
+bool narrow_block(const double* x, int64_t i0, int64_t i1, T* out) {
+  const double hi = (double)std::numeric_limits<T>::max();
+  bool ok = true;
+  for (int64_t i = i0; i < i1; ++i) {
+    const double v = x[i];
+    const bool in = v >= 0.0 && v <= hi;  // false for NaN
+    const T t = in ? (T)v : (T)0;
+    ok &= in && (double)t == v;
+    out[i] = t;
+  }
+  return ok;
+}
+}  // namespace
+
 
 // ------------------------------------------------------------------ NCCL ---
 // Loaded on first use so the library (and single-GPU plans) do not depend on
@@ -122,6 +147,9 @@ struct fcm_plan {
   int profile = 0;  // record the loop kernel's per-CTA timeline
   int seed_pass = 1;  // loop kernel generates the seeded u_0 as its pass 0
   int recompute = 0;  // loop kernel: "effective" mode, passes >= 2 stream x only
+  std::vector<double> deltas;  // delta_1..delta_k of the last fcm_run
+  std::vector<double> res_tab_u;  // the 256-row result table of the last fcm_download_table
+  int32_t res_tab_l[256] = {};
   unsigned debug_delay_ns = 0;  // loop kernel: one CTA per pass sleeps after the grid barrier (tests)
   int debug_shared_parts = 0;   // loop kernel: single tile-partial buffer (the racy round-1 layout; tests)
   unsigned run_counter = 0;  // fcm_run calls (mailbox tags); identical on every rank
@@ -245,7 +273,7 @@ int setup_shard(fcm_plan* p, Shard& s) {
   CK(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&s.ev_pass, cudaEventDisableTiming));
   const int nf = nf_of(p->c);
-  const size_t xsz = p->xkind == XK_U8 ? 1 : 8;
+  const size_t xsz = xkind_bytes(p->xkind);
   int rc;
   uint8_t* xb = nullptr;
   if ((rc = dalloc(p, s, &xb, s.g.plane * xsz))) return rc;
@@ -630,7 +658,7 @@ int fcm_device_count(int32_t* count) {
 
 static int validate_create(int64_t n, int32_t c, int32_t x_kind) {
   if (n < 1 || c < 2 || c > kCMaxSupported || n < c) return FCM_E_ARG;
-  if (x_kind != FCM_X_U8 && x_kind != FCM_X_F64) return FCM_E_ARG;
+  if (x_kind != FCM_X_U8 && x_kind != FCM_X_U16 && x_kind != FCM_X_F64) return FCM_E_ARG;
   if (n > (int64_t)8192 * (int64_t(1) << 30)) return FCM_E_ARG;
   return FCM_OK;
 }
@@ -644,7 +672,7 @@ int fcm_plan_create(fcm_plan** out, int64_t n, int32_t c, int32_t x_kind, int32_
   fcm_plan* p = new fcm_plan();
   p->n_global = n;
   p->c = c;
-  p->xkind = x_kind == FCM_X_U8 ? XK_U8 : XK_F64;
+  p->xkind = x_kind == FCM_X_U8 ? XK_U8 : (x_kind == FCM_X_U16 ? XK_U16 : XK_F64);
   p->nshards = nshards;
   p->nranks = nshards;
   Geometry base{};
@@ -698,7 +726,7 @@ int fcm_plan_create_rank(fcm_plan** out, int64_t n_global, int32_t c, int32_t x_
   fcm_plan* p = new fcm_plan();
   p->n_global = n_global;
   p->c = c;
-  p->xkind = x_kind == FCM_X_U8 ? XK_U8 : XK_F64;
+  p->xkind = x_kind == FCM_X_U8 ? XK_U8 : (x_kind == FCM_X_U16 ? XK_U16 : XK_F64);
   p->nshards = 1;
   p->nranks = nranks;
   p->rank = rank;
@@ -792,7 +820,7 @@ int fcm_plan_info(const fcm_plan* p, int64_t* info, int32_t count) {
 
 int fcm_upload_pixels(fcm_plan* p, const void* x) {
   if (check_plan(p) || !x) return FCM_E_ARG;
-  const size_t xsz = p->xkind == XK_U8 ? 1 : 8;
+  const size_t xsz = xkind_bytes(p->xkind);
   const int64_t host0 = p->nranks > p->nshards ? p->sh[0].g.voxel0 : 0;  // rank plans: host buffers hold the rank slice
   for (int i = 0; i < p->nshards; ++i) {
     Shard& s = p->sh[i];
@@ -859,7 +887,7 @@ int fcm_run(fcm_plan* p, double m, double eps, int32_t max_iters, double* v_out,
     Shard& s = p->sh[i];
     CK(cudaSetDevice(s.device));
     if (s.trace_cap < max_iters) {
-      int rc = dalloc(p, s, &s.trace, (size_t)max_iters);
+      int rc = dalloc(p, s, &s.trace, (size_t)2 * max_iters);  // objective, then delta trace
       if (rc) return rc;
       s.trace_cap = max_iters;
     }
@@ -878,7 +906,9 @@ int fcm_run(fcm_plan* p, double m, double eps, int32_t max_iters, double* v_out,
   const bool single = p->nshards == 1 && !p->use_nccl && !p->timing;
   // loop kernel: single-process plans (mailboxes in process for >1 shard) or
   // multi-process ranks whose peer mailboxes are mapped
-  bool loop = p->use_loop && !p->timing && p->variant != 1 && (!p->use_nccl || p->p2p_ready);
+  // (17 <= c <= 32: per-pass register-staged kernels only -- no stage ring
+  // holds that many membership planes)
+  bool loop = p->use_loop && !p->timing && p->variant != 1 && p->c <= 16 && (!p->use_nccl || p->p2p_ready);
   for (int i = 0; i < p->nshards; ++i) loop = loop && p->sh[i].g.tiles_local > 0;
   const bool graph = !loop && single && p->use_graph;
   if (!loop && p->nranks > p->nshards && !p->use_nccl)
@@ -1030,6 +1060,9 @@ int fcm_run(fcm_plan* p, double m, double eps, int32_t max_iters, double* v_out,
   if (v_out) memcpy(v_out, h.v, sizeof(double) * p->c);
   if (trace_out && h.iter > 0)
     CK(cudaMemcpy(trace_out, s0.trace, sizeof(double) * h.iter, cudaMemcpyDeviceToHost));
+  p->deltas.assign((size_t)std::max(h.iter, 0), 0.0);
+  if (h.iter > 0)
+    CK(cudaMemcpy(p->deltas.data(), s0.trace + max_iters, sizeof(double) * h.iter, cudaMemcpyDeviceToHost));
   if (!h.done) return fail(p, FCM_E_STATE, "loop ended without the done flag");
   if (h.dead == -2) return fail(p, FCM_E_STATE, "device loop watchdog fired (internal error)");
   if (h.dead == -3) return fail(p, FCM_E_STATE, "loop kernel grid barrier timed out (internal error)");
@@ -1146,6 +1179,8 @@ int fcm_download_table(fcm_plan* p, const uint8_t* x_host, double* u_out, int32_
   CK(cudaMemcpyAsync(tab.data(), s0.tab_u, sizeof(double) * tab.size(), cudaMemcpyDeviceToHost, s0.stream));
   CK(cudaMemcpyAsync(ltab, s0.tab_l, sizeof(ltab), cudaMemcpyDeviceToHost, s0.stream));
   CK(cudaStreamSynchronize(s0.stream));
+  p->res_tab_u = tab;  // fcm_result_table
+  memcpy(p->res_tab_l, ltab, sizeof ltab);
   // host expansion over the plan's voxel range (rank plans: the rank slice)
   int64_t n = 0;
   for (int i = 0; i < p->nshards; ++i) n += p->sh[i].g.n_local;
@@ -1168,11 +1203,48 @@ int fcm_download_table(fcm_plan* p, const uint8_t* x_host, double* u_out, int32_
   return FCM_OK;
 }
 
+int fcm_result_table(const fcm_plan* p, double* u_tab, int32_t* l_tab) {
+  if (!p || (!u_tab && !l_tab)) return FCM_E_ARG;
+  if (p->res_tab_u.empty()) return FCM_E_STATE;
+  if (u_tab) memcpy(u_tab, p->res_tab_u.data(), sizeof(double) * p->res_tab_u.size());
+  if (l_tab) memcpy(l_tab, p->res_tab_l, sizeof p->res_tab_l);
+  return FCM_OK;
+}
+
+
+int fcm_narrow_pixels(const double* x, int64_t n, int32_t x_kind, void* out, int32_t nthreads) {
+  if ((!x || !out) && n > 0) return FCM_E_ARG;
+  if (n < 0 || (x_kind != XK_U8 && x_kind != XK_U16)) return FCM_E_ARG;
+  int T = nthreads > 0 ? nthreads : (int)std::thread::hardware_concurrency();
+  T = (int)std::max<int64_t>(1, std::min<int64_t>(T, std::max<int64_t>(1, n >> 18)));
+  const int64_t chunk = (n + T - 1) / T;
+  std::vector<char> ok(T, 1);
+  auto work = [&](int t) {
+    const int64_t i0 = t * chunk, i1 = std::min(n, i0 + chunk);
+    if (i0 >= i1) return;
+    ok[t] = x_kind == XK_U8 ? narrow_block(x, i0, i1, (uint8_t*)out) : narrow_block(x, i0, i1, (uint16_t*)out);
+  };
+  std::vector<std::thread> th;
+  for (int t = 1; t < T; ++t) th.emplace_back(work, t);
+  work(0);
+  for (auto& t : th) t.join();
+  for (int t = 0; t < T; ++t)
+    if (!ok[t]) return FCM_E_ARG;
+  return FCM_OK;
+}
+
 int fcm_last_timing(const fcm_plan* p, double* out, int32_t count) {
   if (!p || !out) return FCM_E_ARG;
   const double v[] = {p->t_loop_ms, p->t_pass_ms, p->t_pro_ms, (double)p->passes_launched,
                       (double)p->passes_done, (double)p->seeded_in_loop};
   for (int i = 0; i < count && i < (int)(sizeof v / sizeof v[0]); ++i) out[i] = v[i];
+  return FCM_OK;
+}
+
+int fcm_delta_trace(const fcm_plan* p, double* out, int32_t count) {
+  if (!p || !out || count < 0) return FCM_E_ARG;
+  if (p->deltas.empty()) return FCM_E_STATE;
+  for (int i = 0; i < count && i < (int)p->deltas.size(); ++i) out[i] = p->deltas[i];
   return FCM_OK;
 }
 
@@ -1349,7 +1421,7 @@ int fcm_update_centers(const double* x, const double* u, double* v_out, int64_t 
     tmpl.dead = -1;
     Shard& s = p->sh[0];
     cudaSetDevice(s.device);
-    if (s.trace_cap < 1) rc = dalloc(p, s, &s.trace, 1), s.trace_cap = 1;
+    if (s.trace_cap < 1) rc = dalloc(p, s, &s.trace, 2), s.trace_cap = 1;
     if (!rc) {
       *p->host_tmpl = tmpl;
       cudaMemcpyAsync(s.ctl, p->host_tmpl, sizeof tmpl, cudaMemcpyHostToDevice, s.stream);

@@ -11,6 +11,7 @@ namespace fcm {
   extern template cudaError_t launch_prologue_c<C>(int, int, bool, const PassArgs&, int, cudaStream_t); \
   extern template cudaError_t launch_epilogue_c<C>(int, int, const EpilogueArgs&, int, cudaStream_t);
 FCM_EXTERN(2) FCM_EXTERN(3) FCM_EXTERN(4) FCM_EXTERN(5) FCM_EXTERN(6) FCM_EXTERN(7) FCM_EXTERN(8) FCM_EXTERN(16)
+FCM_EXTERN(32)
 
 __global__ void finalize_kernel(FinalizeArgs a) {
   // Combine the N rank roots (already gathered, rank-major) in the binary
@@ -34,7 +35,7 @@ __global__ void finalize_kernel(FinalizeArgs a) {
 
 
 #define FCM_SWITCH(CALL)          \
-  switch (c <= 8 ? c : 16) {      \
+  switch (c <= 8 ? c : (c <= 16 ? 16 : 32)) { \
     case 2: return CALL(2);       \
     case 3: return CALL(3);       \
     case 4: return CALL(4);       \
@@ -43,6 +44,7 @@ __global__ void finalize_kernel(FinalizeArgs a) {
     case 7: return CALL(7);       \
     case 8: return CALL(8);       \
     case 16: return CALL(16);     \
+    case 32: return CALL(32);     \
     default: return cudaErrorInvalidValue; \
   }
 

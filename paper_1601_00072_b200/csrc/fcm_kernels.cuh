@@ -57,6 +57,7 @@ __device__ inline void finalize_body(Control* ctl, const double* root, int c, do
     const int k = ctl->iter + 1;
     ctl->iter = k;
     trace[k - 1] = root[2 * c];
+    trace[max_iters + k - 1] = root[2 * c + 1];  // delta trace (second half of the buffer)
     ctl->delta = root[2 * c + 1];
     if (root[2 * c + 1] < eps) {  // core.py:129-131
       ctl->converged = 1;
@@ -271,6 +272,17 @@ struct XLoad<uint8_t> {
     for (int q = 0; q < 4; ++q) xd[q] = (double)((w >> (8 * q)) & 0xffu);
   }
   static __device__ __forceinline__ double load1(const uint8_t* x, int64_t i) { return (double)x[i]; }
+};
+template <>
+struct XLoad<uint16_t> {
+  static __device__ __forceinline__ void load4(const uint16_t* x, int64_t i, double* xd) {
+    const uint2 w = __ldg(reinterpret_cast<const uint2*>(x + i));
+    xd[0] = (double)(w.x & 0xffffu);
+    xd[1] = (double)(w.x >> 16);
+    xd[2] = (double)(w.y & 0xffffu);
+    xd[3] = (double)(w.y >> 16);
+  }
+  static __device__ __forceinline__ double load1(const uint16_t* x, int64_t i) { return (double)x[i]; }
 };
 template <>
 struct XLoad<double> {
@@ -522,26 +534,34 @@ inline int occupancy_grid(KernelPtr k, int tiles, int sms) {
 }
 
 // One translation unit per cluster count C instantiates these (fcm_inst_c*.cu).
+// Per-voxel math of a plan: m == 2 product form (C <= 8) or the general
+// robust form.  C == 32 (17 <= c <= 32) runs the register-staged pass kernel
+// only: no shared-memory stage holds 17..32 membership planes of a chunk.
 template <int C>
 cudaError_t launch_pass_c(int xkind, int mode, const PassArgs& a, int sms, cudaStream_t st,
                           int* grid_out, int variant, int force_grid) {
   constexpr int MD = C <= 8 ? MODE_M2 : MODE_GEN;
   const bool m2 = (mode == MODE_M2) && C <= 8;
-  if (variant == 0 || variant == 2 || variant == 3) {  // TMA bulk pipeline (production)
-    if (xkind == XK_U8) {
-      // uint8 pixels: m == 2 -> fused product form; any other m (or variant 2)
-      // -> per-pass intensity table (C <= 8); variant 3 -> direct math always.
-      if (C <= 8 && variant != 3 && (variant == 2 || !m2))
-        return launch_pass_tma<uint8_t, C, (C <= 8 ? MODE_LUT : MODE_GEN)>(a, sms, st, grid_out, force_grid);
-      if (C <= 8 && m2 && variant == 0)
-        return launch_pass_tma<uint8_t, C, (C <= 8 ? MODE_LUT2 : MODE_GEN)>(a, sms, st, grid_out, force_grid);
-      return m2 ? launch_pass_tma<uint8_t, C, MD>(a, sms, st, grid_out, force_grid)
-                : launch_pass_tma<uint8_t, C, MODE_GEN>(a, sms, st, grid_out, force_grid);
+  if constexpr (C <= 16) {
+    if (variant == 0 || variant == 2 || variant == 3) {  // TMA bulk pipeline (production)
+      if (xkind == XK_U8) {
+        // uint8 pixels: m == 2 -> fused product form; any other m (or variant 2)
+        // -> per-pass intensity table (C <= 8); variant 3 -> direct math always.
+        if (C <= 8 && variant != 3 && (variant == 2 || !m2))
+          return launch_pass_tma<uint8_t, C, (C <= 8 ? MODE_LUT : MODE_GEN)>(a, sms, st, grid_out, force_grid);
+        if (C <= 8 && m2 && variant == 0)
+          return launch_pass_tma<uint8_t, C, (C <= 8 ? MODE_LUT2 : MODE_GEN)>(a, sms, st, grid_out, force_grid);
+        return m2 ? launch_pass_tma<uint8_t, C, MD>(a, sms, st, grid_out, force_grid)
+                  : launch_pass_tma<uint8_t, C, MODE_GEN>(a, sms, st, grid_out, force_grid);
+      }
+      if (xkind == XK_U16)
+        return m2 ? launch_pass_tma<uint16_t, C, MD>(a, sms, st, grid_out, force_grid)
+                  : launch_pass_tma<uint16_t, C, MODE_GEN>(a, sms, st, grid_out, force_grid);
+      return m2 ? launch_pass_tma<double, C, MD>(a, sms, st, grid_out, force_grid)
+                : launch_pass_tma<double, C, MODE_GEN>(a, sms, st, grid_out, force_grid);
     }
-    return m2 ? launch_pass_tma<double, C, MD>(a, sms, st, grid_out, force_grid)
-              : launch_pass_tma<double, C, MODE_GEN>(a, sms, st, grid_out, force_grid);
   }
-  int grid = 0;  // variant 1: register-staged LDG/STG kernel (kept for A/B)
+  int grid = 0;  // variant 1 / C == 32: register-staged LDG/STG kernel
   auto go = [&](auto k) {
     grid = force_grid > 0 ? std::min(force_grid, a.g.tiles_local) : occupancy_grid(k, a.g.tiles_local, sms);
     k<<<grid, kThreads, 0, st>>>(a);
@@ -549,6 +569,9 @@ cudaError_t launch_pass_c(int xkind, int mode, const PassArgs& a, int sms, cudaS
   if (xkind == XK_U8) {
     if (m2) go(pass_kernel<uint8_t, C, MD>);
     else go(pass_kernel<uint8_t, C, MODE_GEN>);
+  } else if (xkind == XK_U16) {
+    if (m2) go(pass_kernel<uint16_t, C, MD>);
+    else go(pass_kernel<uint16_t, C, MODE_GEN>);
   } else {
     if (m2) go(pass_kernel<double, C, MD>);
     else go(pass_kernel<double, C, MODE_GEN>);
@@ -560,19 +583,26 @@ cudaError_t launch_pass_c(int xkind, int mode, const PassArgs& a, int sms, cudaS
 template <int C>
 cudaError_t launch_loop_c(int xkind, int mode, const PassArgs& a, int sms, cudaStream_t st, int* grid_out,
                           int variant, int force_grid, int share) {
-  constexpr int MD = C <= 8 ? MODE_M2 : MODE_GEN;
-  const bool m2 = (mode == MODE_M2) && C <= 8;
-  if (variant == 1) return cudaErrorNotSupported;  // the LDG kernel has no loop form
-  if (xkind == XK_U8) {
-    if (C <= 8 && variant != 3 && (variant == 2 || !m2))
-      return launch_loop_tma<uint8_t, C, (C <= 8 ? MODE_LUT : MODE_GEN)>(a, sms, st, grid_out, force_grid, share);
-    if (C <= 8 && m2 && variant == 0)
-      return launch_loop_tma<uint8_t, C, (C <= 8 ? MODE_LUT2 : MODE_GEN)>(a, sms, st, grid_out, force_grid, share);
-    return m2 ? launch_loop_tma<uint8_t, C, MD>(a, sms, st, grid_out, force_grid, share)
-              : launch_loop_tma<uint8_t, C, MODE_GEN>(a, sms, st, grid_out, force_grid, share);
+  if constexpr (C > 16) {
+    return cudaErrorNotSupported;  // per-pass launches (register-staged kernel)
+  } else {
+    constexpr int MD = C <= 8 ? MODE_M2 : MODE_GEN;
+    const bool m2 = (mode == MODE_M2) && C <= 8;
+    if (variant == 1) return cudaErrorNotSupported;  // the LDG kernel has no loop form
+    if (xkind == XK_U8) {
+      if (C <= 8 && variant != 3 && (variant == 2 || !m2))
+        return launch_loop_tma<uint8_t, C, (C <= 8 ? MODE_LUT : MODE_GEN)>(a, sms, st, grid_out, force_grid, share);
+      if (C <= 8 && m2 && variant == 0)
+        return launch_loop_tma<uint8_t, C, (C <= 8 ? MODE_LUT2 : MODE_GEN)>(a, sms, st, grid_out, force_grid, share);
+      return m2 ? launch_loop_tma<uint8_t, C, MD>(a, sms, st, grid_out, force_grid, share)
+                : launch_loop_tma<uint8_t, C, MODE_GEN>(a, sms, st, grid_out, force_grid, share);
+    }
+    if (xkind == XK_U16)
+      return m2 ? launch_loop_tma<uint16_t, C, MD>(a, sms, st, grid_out, force_grid, share)
+                : launch_loop_tma<uint16_t, C, MODE_GEN>(a, sms, st, grid_out, force_grid, share);
+    return m2 ? launch_loop_tma<double, C, MD>(a, sms, st, grid_out, force_grid, share)
+              : launch_loop_tma<double, C, MODE_GEN>(a, sms, st, grid_out, force_grid, share);
   }
-  return m2 ? launch_loop_tma<double, C, MD>(a, sms, st, grid_out, force_grid, share)
-            : launch_loop_tma<double, C, MODE_GEN>(a, sms, st, grid_out, force_grid, share);
 }
 
 template <int C>
@@ -584,6 +614,9 @@ cudaError_t launch_prologue_c(int xkind, int mode, bool from_seed, const PassArg
   if (xkind == XK_U8) {
     if (from_seed) m2 ? go(prologue_kernel<uint8_t, C, MD, true>) : go(prologue_kernel<uint8_t, C, MODE_GEN, true>);
     else m2 ? go(prologue_kernel<uint8_t, C, MD, false>) : go(prologue_kernel<uint8_t, C, MODE_GEN, false>);
+  } else if (xkind == XK_U16) {
+    if (from_seed) m2 ? go(prologue_kernel<uint16_t, C, MD, true>) : go(prologue_kernel<uint16_t, C, MODE_GEN, true>);
+    else m2 ? go(prologue_kernel<uint16_t, C, MD, false>) : go(prologue_kernel<uint16_t, C, MODE_GEN, false>);
   } else {
     if (from_seed) m2 ? go(prologue_kernel<double, C, MD, true>) : go(prologue_kernel<double, C, MODE_GEN, true>);
     else m2 ? go(prologue_kernel<double, C, MD, false>) : go(prologue_kernel<double, C, MODE_GEN, false>);
@@ -597,11 +630,15 @@ cudaError_t launch_epilogue_c(int xkind, int mode, const EpilogueArgs& a, int sm
   long long cap = (long long)sms * 8;
   int grid = (int)(want < cap ? (want < 1 ? 1 : want) : cap);
   const bool m2 = (mode == MODE_M2) && C <= 8;
+  constexpr int MD = C <= 8 ? MODE_M2 : MODE_GEN;
   if (xkind == XK_U8) {
-    if (m2) epilogue_kernel<uint8_t, C, (C <= 8 ? MODE_M2 : MODE_GEN)><<<grid, kThreads, 0, st>>>(a);
+    if (m2) epilogue_kernel<uint8_t, C, MD><<<grid, kThreads, 0, st>>>(a);
     else epilogue_kernel<uint8_t, C, MODE_GEN><<<grid, kThreads, 0, st>>>(a);
+  } else if (xkind == XK_U16) {
+    if (m2) epilogue_kernel<uint16_t, C, MD><<<grid, kThreads, 0, st>>>(a);
+    else epilogue_kernel<uint16_t, C, MODE_GEN><<<grid, kThreads, 0, st>>>(a);
   } else {
-    if (m2) epilogue_kernel<double, C, (C <= 8 ? MODE_M2 : MODE_GEN)><<<grid, kThreads, 0, st>>>(a);
+    if (m2) epilogue_kernel<double, C, MD><<<grid, kThreads, 0, st>>>(a);
     else epilogue_kernel<double, C, MODE_GEN><<<grid, kThreads, 0, st>>>(a);
   }
   return cudaGetLastError();

@@ -8,7 +8,7 @@
 
 namespace fcm {
 
-enum { XK_U8 = 0, XK_F64 = 2 };
+enum { XK_U8 = 0, XK_U16 = 1, XK_F64 = 2 };
 
 struct PassArgs {
   const void* x;          // pixels of this rank, padded to the plane length
@@ -29,7 +29,7 @@ struct PassArgs {
   unsigned* node_cnt[kMaxLevels + 1]; // level l >= 1: [noct][nodes[l]] arrival counters
   double* rank_root;      // [nf]
   Control* ctl;
-  double* trace;          // [max_iters]
+  double* trace;          // [2][max_iters]: objective J_k, then delta_k
   cudaGraphConditionalHandle cond;  // device-side loop: while(cond) { pass } (graph mode)
   int use_cond;
   int finalize_local;     // 1: the CTA completing the rank root finalizes (single-rank jobs)

@@ -95,7 +95,8 @@ __device__ __forceinline__ double f32_to_f64_fast(float f) {
   return __hiloint2double((int)((b >> 3) + 0x38000000u), (int)(b << 29));
 }
 
-// uint8 intensity -> double via the 2^52 magic constant (one DADD).
+// uint8 (or any 32-bit unsigned) intensity -> double via the 2^52 magic
+// constant (one DADD).
 __device__ __forceinline__ double u8_to_f64(uint32_t byte) {
   return __hiloint2double(0x43300000, (int)byte) - 4503599627370496.0;
 }
@@ -527,6 +528,12 @@ __device__ __forceinline__ void tma_consume_seed(const PassArgs& a, uint8_t* sme
           for (int k = 0; k < 8; ++k) pm[k] |= (b >> 5) == (uint32_t)k ? bit : 0u;
         }
       }
+    } else if (sizeof(XT) == 2) {
+      const uint2 w = *reinterpret_cast<const uint2*>(st + tid * 8);
+      xd[0] = u8_to_f64(w.x & 0xffffu);  // (exact for any 32-bit unsigned value)
+      xd[1] = u8_to_f64(w.x >> 16);
+      xd[2] = u8_to_f64(w.y & 0xffffu);
+      xd[3] = u8_to_f64(w.y >> 16);
     } else {
       const double2 p0 = *reinterpret_cast<const double2*>(st + tid * 32);
       const double2 p1 = *reinterpret_cast<const double2*>(st + tid * 32 + 16);
@@ -617,6 +624,12 @@ __device__ __forceinline__ void tma_consume(const PassArgs& a, uint8_t* smem, Pi
       const uint32_t w = *reinterpret_cast<const uint32_t*>(st + tid * 4);
 #pragma unroll
       for (int q = 0; q < 4; ++q) xd[q] = u8_to_f64((w >> (8 * q)) & 0xffu);
+    } else if (sizeof(XT) == 2) {
+      const uint2 w = *reinterpret_cast<const uint2*>(st + tid * 8);
+      xd[0] = u8_to_f64(w.x & 0xffffu);  // (exact for any 32-bit unsigned value)
+      xd[1] = u8_to_f64(w.x >> 16);
+      xd[2] = u8_to_f64(w.y & 0xffffu);
+      xd[3] = u8_to_f64(w.y >> 16);
     } else {
       const double2 p0 = *reinterpret_cast<const double2*>(st + tid * 32);
       const double2 p1 = *reinterpret_cast<const double2*>(st + tid * 32 + 16);

@@ -440,6 +440,7 @@ __device__ __forceinline__ void finalize_loop(const PassArgs& a, const double* r
     }
     ctl->iter = k;
     a.trace[k - 1] = root[2 * c];
+    a.trace[a.max_iters + k - 1] = delta;  // delta trace (second half of the buffer)
     ctl->delta = delta;
     ctl->converged = conv ? 1 : 0;
     ctl->dead = dead;

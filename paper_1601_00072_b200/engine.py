@@ -20,6 +20,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+import threading
 
 import numpy as np
 
@@ -28,21 +29,32 @@ from ._lib import check, lib, ptr
 from .errors import DegenerateClusterError, DimensionMismatchError, FcmError, InvalidConfigError
 from .types import ClusterCenters, FcmConfig, FcmResult, GrayImage, LabelMap, MembershipMatrix
 
-C_MAX = 16
+C_MAX = 32
 
 
 def pixel_kind(pixels: np.ndarray):
     """Pick the narrowest exact device representation of the pixels.
 
     Integer intensities 0..255 travel and live in HBM as uint8 (every
-    BASELINE config); anything else stays float64 (types.py:38-41 accepts any
-    finite non-negative value).  Returns (FCM_X_*, contiguous array).
+    BASELINE config), 256..65535 as uint16 (16-bit PGM rasters,
+    imgio.py:102-110); anything else stays float64 (types.py:38-41 accepts
+    any finite non-negative value).  float64 input is checked and narrowed in
+    one multi-threaded pass in the library (fcm_narrow_pixels).  Returns
+    (FCM_X_*, contiguous array).
     """
     if pixels.dtype == np.uint8:
         return _lib.FCM_X_U8, np.ascontiguousarray(pixels)
-    x = np.ascontiguousarray(pixels, dtype=np.float64)
-    if x.size and x.max() <= 255.0 and x.min() >= 0.0 and np.array_equal(x, np.rint(x)):
+    if pixels.dtype == np.uint16:
+        x = np.ascontiguousarray(pixels)
+        if x.size and int(x.max()) > 255:
+            return _lib.FCM_X_U16, x
         return _lib.FCM_X_U8, x.astype(np.uint8)
+    x = np.ascontiguousarray(pixels, dtype=np.float64)
+    n = x.shape[0]
+    for kind, dt in ((_lib.FCM_X_U8, np.uint8), (_lib.FCM_X_U16, np.uint16)):
+        out = np.empty(n, dtype=dt)
+        if lib().fcm_narrow_pixels(ptr(x), n, kind, ptr(out), 0) == _lib.FCM_OK:
+            return kind, out
     return _lib.FCM_X_F64, x
 
 
@@ -156,8 +168,8 @@ class FcmPlan:
 
     # -- data ------------------------------------------------------------
     def upload_pixels(self, x: np.ndarray):
-        """Pixels of this plan's voxel range, uint8 (FCM_X_U8) or float64."""
-        want = np.uint8 if self.x_kind == _lib.FCM_X_U8 else np.float64
+        """Pixels of this plan's voxel range: uint8 (FCM_X_U8), uint16 (FCM_X_U16) or float64."""
+        want = {_lib.FCM_X_U8: np.uint8, _lib.FCM_X_U16: np.uint16}.get(self.x_kind, np.float64)
         x = np.ascontiguousarray(x, dtype=want)
         check(lib().fcm_upload_pixels(self._h, ptr(x)), self._h, "fcm_upload_pixels")
 
@@ -211,6 +223,13 @@ class FcmPlan:
               "fcm_download_table")
         return u, lab
 
+    def result_table(self):
+        """(u_tab [256, c] float64, l_tab [256] int32): the result table of the last download_table."""
+        u = np.empty(256 * self.c, dtype=np.float64)
+        lab = np.empty(256, dtype=np.int32)
+        check(lib().fcm_result_table(self._h, ptr(u), ptr(lab)), self._h, "fcm_result_table")
+        return u.reshape(256, self.c), lab
+
     def profile(self) -> np.ndarray:
         """Loop-kernel timeline of the last run (FCM_OPT_PROFILE): array [pass, cta, slot]
         with slots 0 start, 1 claims done, 2 consumers done, 3 barrier released (ns), 4 tiles."""
@@ -251,6 +270,12 @@ class FcmPlan:
         """|pred==p| for each cluster p."""
         return self._mask_stats(np.zeros(self.n_local, dtype=bool))[self.c + 1:]
 
+    def delta_trace(self, iterations: int) -> np.ndarray:
+        """delta_1..delta_k of the last run (what the stop test compared with epsilon)."""
+        d = np.zeros(iterations, dtype=np.float64)
+        check(lib().fcm_delta_trace(self._h, ptr(d), int(iterations)), self._h, "fcm_delta_trace")
+        return d
+
     def timing(self) -> dict:
         keys = ("loop_ms", "pass_ms", "prologue_ms", "passes_launched", "passes", "seeded_in_loop")
         buf = (ctypes.c_double * len(keys))()
@@ -261,27 +286,83 @@ class FcmPlan:
 # ----------------------------------------------------------------- engine --
 def _check_c(c: int):
     if c > C_MAX:
-        raise InvalidConfigError(f"the GPU path supports c <= {C_MAX}, got {c}")
+        raise InvalidConfigError(f"the GPU path supports c <= {C_MAX} (kernel payload), got {c}")
+
+
+# One cached plan per host thread (plans are not re-entrant): repeated solves
+# of the same shape -- the reference's bench loop (bench.py:49-59, 96-106)
+# and every caller that segments a series of same-sized volumes -- reuse the
+# device buffers instead of allocating and freeing them per call.
+_plans = threading.local()
+
+
+def _cached_plan(n: int, c: int, kind: int, devices) -> FcmPlan:
+    key = (int(n), int(c), int(kind), tuple(_devices(devices)))
+    ent = getattr(_plans, "entry", None)
+    if ent is not None and ent[0] == key and ent[1]._h:
+        return ent[1]
+    release_cached_plans()
+    plan = FcmPlan(n, c, kind, devices)
+    _plans.entry = (key, plan)
+    return plan
+
+
+def release_cached_plans() -> None:
+    """Free the device memory of this thread's cached plan (run_fcm_gpu / _iterate)."""
+    ent = getattr(_plans, "entry", None)
+    _plans.entry = None
+    if ent is not None:
+        ent[1].close()
+
+
+def _solve(plan: FcmPlan, xx, kind, cfg: FcmConfig, u0=None):
+    """Upload, run and download on `plan`; returns (v, trace, k, conv, u, labels, table).
+    A failed run (other than a dead cluster) drops the plan from the cache."""
+    try:
+        plan.upload_pixels(xx)
+        if u0 is None:
+            plan.init_membership(cfg.seed64)
+        else:
+            plan.upload_membership(u0)
+        v, trace, k, conv = plan.run(cfg.m, cfg.epsilon, cfg.max_iters)
+        table = None
+        if kind == _lib.FCM_X_U8:
+            # 8-bit pixels: at most 256 distinct result rows -- copy the table,
+            # expand on the host (identical arrays, ~n*8c fewer PCIe bytes)
+            u, labels = plan.download_table(xx)
+            table = plan.result_table()
+        else:
+            u, labels = plan.download()
+    except DegenerateClusterError:
+        raise
+    except BaseException:
+        ent = getattr(_plans, "entry", None)
+        if ent is not None and ent[1] is plan:
+            release_cached_plans()
+        raise
+    return v, trace, k, conv, u, labels, table
 
 
 def _iterate(x: np.ndarray, u0: np.ndarray | None, cfg: FcmConfig, devices=None, seed: int | None = None):
     """Device counterpart of core._iterate (core.py:105-132).
 
-    x: pixels (float64 or uint8); u0: AoS float64 start, or None with `seed`
-    to generate the reference's seeded start on the device.  Returns
+    x: pixels (float64, uint8 or uint16); u0: AoS float64 start (consumed
+    like the reference's scratch, here only read), or None with `seed` to
+    generate the reference's seeded start on the device.  Returns
     (v, u_final, iterations, trace, converged) like the reference.
     """
     _check_c(cfg.c)
     kind, xx = pixel_kind(np.asarray(x))
     n = xx.shape[0]
-    with FcmPlan(n, cfg.c, kind, devices) as plan:
-        plan.upload_pixels(xx)
-        if u0 is None:
-            plan.init_membership(cfg.seed64 if seed is None else seed)
-        else:
-            plan.upload_membership(u0)
-        v, trace, k, conv = plan.run(cfg.m, cfg.epsilon, cfg.max_iters)
-        u, _ = plan.download(membership=True, labels=False)
+    if u0 is not None:
+        u0 = np.ascontiguousarray(u0, dtype=np.float64)
+        if u0.shape[0] != n * cfg.c:
+            raise DimensionMismatchError(f"initial membership has {u0.shape[0]} entries, expected {n * cfg.c}")
+    if u0 is None and seed is not None:
+        cfg = FcmConfig(c=cfg.c, m=cfg.m, epsilon=cfg.epsilon, max_iters=cfg.max_iters, seed=seed,
+                        block_size=cfg.block_size)
+    plan = _cached_plan(n, cfg.c, kind, devices)
+    v, trace, k, conv, u, _, _ = _solve(plan, xx, kind, cfg, u0)
     return v, u, k, list(trace), conv
 
 
@@ -292,7 +373,8 @@ def run_fcm_gpu(img: GrayImage, cfg: FcmConfig, devices=None,
     `img` is a GrayImage or an imgio.PgmImage (integer raster, no float64
     expansion).  keep_plan=True returns (FcmResult, FcmPlan) with the plan's
     labels still resident for the device-side metrics (metrics.dsc_report_gpu);
-    the caller closes the plan.
+    the caller closes the plan.  Otherwise the thread's cached plan is reused
+    (release_cached_plans() frees it).
 
     Same seeded initialization as the reference engines (SplitMix64, generated
     on the device), same convergence rule, same result contract.  `devices`
@@ -307,29 +389,29 @@ def run_fcm_gpu(img: GrayImage, cfg: FcmConfig, devices=None,
         raise DimensionMismatchError(
             f"initial membership is {initial_membership.n}x{initial_membership.c}, expected {n}x{cfg.c}")
     # a PgmImage (imgio.read_pgm_raster) hands its integer raster over as is:
-    # 8-bit images reach HBM at 1 B per voxel without a float64 copy
+    # 8-bit images reach HBM at 1 B per voxel, 16-bit at 2 B, without a float64 copy
     from .imgio import PgmImage
     kind, xx = pixel_kind(img.raster if isinstance(img, PgmImage) else img.pixels)
-    plan = FcmPlan(n, cfg.c, kind, devices)
+    plan = FcmPlan(n, cfg.c, kind, devices) if keep_plan else _cached_plan(n, cfg.c, kind, devices)
     try:
-        plan.upload_pixels(xx)
-        if initial_membership is None:
-            plan.init_membership(cfg.seed64)
-        else:
-            plan.upload_membership(initial_membership.u)
-        v, trace, k, conv = plan.run(cfg.m, cfg.epsilon, cfg.max_iters)
-        # 8-bit pixels: at most 256 distinct result rows -- copy the table,
-        # expand on the host (identical arrays, ~n*8c fewer PCIe bytes)
-        u, labels = plan.download_table(xx) if kind == _lib.FCM_X_U8 else plan.download()
+        v, trace, k, conv, u, labels, table = _solve(
+            plan, xx, kind, cfg, None if initial_membership is None else initial_membership.u)
     except BaseException:
-        plan.close()
+        if keep_plan:
+            plan.close()
         raise
-    if not keep_plan:
-        plan.close()
+    if table is not None:
+        # every row / label is a copy of a table entry: validating the 256
+        # table rows validates the result (types.py:82-85) without n*c passes
+        membership = MembershipMatrix.from_table_rows(n, cfg.c, u, table[0])
+        label_map = LabelMap.from_table_labels(img.width, img.height, labels, cfg.c, table[1])
+    else:
+        membership = MembershipMatrix(n, cfg.c, u)
+        label_map = LabelMap(img.width, img.height, labels, cfg.c)
     result = FcmResult(
         centers=ClusterCenters(v),
-        membership=MembershipMatrix(n, cfg.c, u),
-        labels=LabelMap(img.width, img.height, labels, cfg.c),
+        membership=membership,
+        labels=label_map,
         iterations=k,
         objective_trace=tuple(float(t) for t in trace),
         converged=conv,

@@ -129,7 +129,7 @@ def runs_fixture():
     c1 = phantom_slice(181, 217).reshape(-1).astype(np.float64)
     for p, cfg in (("C1", fcmseg.FcmConfig(c=3, m=2.0, epsilon=1e-5, seed=0)),
                    ("C1_c8_m15", fcmseg.FcmConfig(c=8, m=1.5, epsilon=1e-5, seed=0))):
-        run_record(p, c1, 181, 217, cfg, "sequential", out, keep_u=(p == "C1"))
+        run_record(p, c1, 181, 217, cfg, "sequential", out, keep_u=True)
         names.append(p)
     out["names"] = np.array(names)
     return out

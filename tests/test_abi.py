@@ -43,7 +43,7 @@ def test_argument_validation_is_host_side():
     assert L.fcm_plan_create(ctypes.byref(h), 2, 3, 0, 1, None) == _lib.FCM_E_ARG
     assert L.fcm_plan_create(ctypes.byref(h), 100, 3, 7, 1, None) == _lib.FCM_E_ARG
     assert L.fcm_plan_create(ctypes.byref(h), 100, 3, 0, 3, None) == _lib.FCM_E_ARG
-    assert L.fcm_plan_create(ctypes.byref(h), 100, 17, 0, 1, None) == _lib.FCM_E_ARG
+    assert L.fcm_plan_create(ctypes.byref(h), 100, 33, 0, 1, None) == _lib.FCM_E_ARG
     assert L.fcm_plan_create_rank(ctypes.byref(h), 100, 3, 0, 0, 2, 2, None) == _lib.FCM_E_ARG
     assert L.fcm_set_option(None, 1, 8) == _lib.FCM_E_ARG
     assert L.fcm_max_abs_diff(None, None, 4, 0, None) == _lib.FCM_E_ARG
@@ -59,12 +59,30 @@ def test_no_gpu_means_loud_failure_not_fallback():
 
 
 def test_pixel_kind_selection():
+    # host-only: fcm_narrow_pixels needs no GPU
     k, a = pkg.pixel_kind(np.array([0.0, 17.0, 255.0]))
+    assert k == _lib.FCM_X_U8 and a.dtype == np.uint8 and a.tolist() == [0, 17, 255]
+    k, a = pkg.pixel_kind(np.array([0.0, 256.0, 65535.0]))
+    assert k == _lib.FCM_X_U16 and a.dtype == np.uint16 and a.tolist() == [0, 256, 65535]
+    for bad in ([0.5, 2.0], [0.0, 65536.0], [1.0, np.nan], [1.0, -1.0], [1.0, np.inf]):
+        k, a = pkg.pixel_kind(np.array(bad))
+        assert k == _lib.FCM_X_F64 and a.dtype == np.float64
+    k, a = pkg.pixel_kind(np.array([3, 200], dtype=np.uint16))  # 16-bit raster, 8-bit values
     assert k == _lib.FCM_X_U8 and a.dtype == np.uint8
-    k, a = pkg.pixel_kind(np.array([0.0, 256.0]))
-    assert k == _lib.FCM_X_F64
-    k, a = pkg.pixel_kind(np.array([0.5, 2.0]))
-    assert k == _lib.FCM_X_F64
+    k, a = pkg.pixel_kind(np.array([3, 300], dtype=np.uint16))
+    assert k == _lib.FCM_X_U16 and a.dtype == np.uint16
+
+
+def test_narrow_pixels_large_multithreaded():
+    rng = np.random.default_rng(3)
+    x = rng.integers(0, 256, 3_000_001).astype(np.float64)
+    k, a = pkg.pixel_kind(x)
+    assert k == _lib.FCM_X_U8 and np.array_equal(a, x.astype(np.uint8))
+    x[2_999_999] = 255.5  # one bad value in the last thread's block
+    assert pkg.pixel_kind(x)[0] == _lib.FCM_X_F64
+    x[2_999_999] = 4095.0
+    k, a = pkg.pixel_kind(x)
+    assert k == _lib.FCM_X_U16 and np.array_equal(a, x.astype(np.uint16))
 
 
 def test_product_path_does_not_import_oracle():

@@ -55,4 +55,4 @@ def test_engine_validation_before_device():
     with pytest.raises(pkg.DimensionMismatchError):
         pkg.run_fcm_gpu(img, pkg.FcmConfig(c=2), initial_membership=pkg.MembershipMatrix(2, 2, [1, 0, 0, 1]))
     with pytest.raises(pkg.InvalidConfigError):
-        pkg.run_fcm_gpu(pkg.GrayImage(20, 1, np.arange(20.0)), pkg.FcmConfig(c=17))
+        pkg.run_fcm_gpu(pkg.GrayImage(40, 1, np.arange(40.0)), pkg.FcmConfig(c=33))
