@@ -76,10 +76,14 @@ typedef enum {
   FCM_OPT_DEBUG_DELAY = 12, /* diagnostics: after every grid barrier of the loop kernel one CTA (a
                               different one each pass) sleeps this many ns (<= 10 ms) before it reads
                               the pass's partials -- results must not change (race test).  0: default */
-  FCM_OPT_DEBUG_SHARED_PARTIALS = 13 /* diagnostics: 1 = every pass of the loop kernel's small-volume
+  FCM_OPT_DEBUG_SHARED_PARTIALS = 13, /* diagnostics: 1 = every pass of the loop kernel's small-volume
                               path publishes its tile partials into the same buffer (the round-1
                               layout, racy under FCM_OPT_DEBUG_DELAY; shows the race test can fail).
                               0: default (two buffers alternated by pass parity) */
+  FCM_OPT_PEER_TIMEOUT_MS = 14 /* multi-rank loop kernel: how long a rank waits for a peer's per-pass
+                              root before failing fcm_run with FCM_E_NCCL naming the missing rank and
+                              pass (default 4000).  Single-process multi-shard plans retry such a
+                              failure with one launch per pass (fcm_last_timing out[6] counts it). */
 } fcm_option;
 
 typedef struct fcm_plan fcm_plan;
@@ -190,7 +194,8 @@ int fcm_mask_overlap(fcm_plan* plan, const uint8_t* mask, int64_t* counts_out);
  * its duration / passes, the seeded start included), prologue-kernel ms
  * (0 when the loop kernel generated u_0 itself), kernel launches of the
  * loop (1 for the loop kernel), passes that did work, 1 if the loop kernel
- * ran the seeded start as its pass 0. */
+ * ran the seeded start as its pass 0, solves of this plan that fell back
+ * from the multi-shard loop kernel to per-pass launches. */
 int fcm_last_timing(const fcm_plan* plan, double* out, int32_t count);
 
 /* delta_1..delta_k of the last fcm_run (out[0..min(count, iterations))):

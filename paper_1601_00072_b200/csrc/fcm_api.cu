@@ -152,6 +152,11 @@ struct fcm_plan {
   int32_t res_tab_l[256] = {};
   unsigned debug_delay_ns = 0;  // loop kernel: one CTA per pass sleeps after the grid barrier (tests)
   int debug_shared_parts = 0;   // loop kernel: single tile-partial buffer (the racy round-1 layout; tests)
+  int64_t peer_timeout_ms = 4000;  // loop kernel, multi-rank: how long to wait for a peer's root
+  bool force_per_pass = false;  // fcm_run retry after a failed multi-shard loop (shards sharing a device)
+  bool looped_last = false;     // the last run_impl ran the loop kernel
+  int loop_fallbacks = 0;       // solves that fell back to per-pass launches
+  bool labels_valid = false;    // device labels belong to the last successful fcm_run
   unsigned run_counter = 0;  // fcm_run calls (mailbox tags); identical on every rank
   bool p2p_ready = false;    // multi-process ranks: peer mailboxes mapped (fcm_connect_peers)
   Mailbox* peer_mbox[kOctants] = {};
@@ -790,6 +795,10 @@ int fcm_set_option(fcm_plan* p, int32_t key, int64_t value) {
       p->debug_delay_ns = (unsigned)value;
       return FCM_OK;
     case FCM_OPT_DEBUG_SHARED_PARTIALS: p->debug_shared_parts = value ? 1 : 0; return FCM_OK;
+    case FCM_OPT_PEER_TIMEOUT_MS:
+      if (value < 0 || value > 3600000) return FCM_E_ARG;
+      p->peer_timeout_ms = value;
+      return FCM_OK;
     case FCM_OPT_L2:
       if (value < 0 || value > 2) return FCM_E_ARG;
       p->l2_mode = (int)value;
@@ -866,10 +875,12 @@ int fcm_upload_membership(fcm_plan* p, const double* u0) {
   return FCM_OK;
 }
 
-int fcm_run(fcm_plan* p, double m, double eps, int32_t max_iters, double* v_out,
-            double* trace_out, int32_t* iterations, int32_t* converged, int32_t* dead_cluster) {
+static int run_impl(fcm_plan* p, double m, double eps, int32_t max_iters, double* v_out,
+                    double* trace_out, int32_t* iterations, int32_t* converged, int32_t* dead_cluster) {
   if (check_plan(p)) return FCM_E_ARG;
   p->run_ok = false;
+  p->labels_valid = false;
+  p->looped_last = false;
   if (!(m > 1.0) || !std::isfinite(m)) return fail(p, FCM_E_ARG, "fuzzifier must be > 1");
   if (!(eps > 0.0 && eps < 1.0)) return fail(p, FCM_E_ARG, "epsilon must lie in (0, 1)");
   if (max_iters < 1) return fail(p, FCM_E_ARG, "max_iters must be >= 1");
@@ -908,7 +919,8 @@ int fcm_run(fcm_plan* p, double m, double eps, int32_t max_iters, double* v_out,
   // multi-process ranks whose peer mailboxes are mapped
   // (17 <= c <= 32: per-pass register-staged kernels only -- no stage ring
   // holds that many membership planes)
-  bool loop = p->use_loop && !p->timing && p->variant != 1 && p->c <= 16 && (!p->use_nccl || p->p2p_ready);
+  bool loop = p->use_loop && !p->force_per_pass && !p->timing && p->variant != 1 && p->c <= 16 &&
+              (!p->use_nccl || p->p2p_ready);
   for (int i = 0; i < p->nshards; ++i) loop = loop && p->sh[i].g.tiles_local > 0;
   const bool graph = !loop && single && p->use_graph;
   if (!loop && p->nranks > p->nshards && !p->use_nccl)
@@ -945,6 +957,7 @@ int fcm_run(fcm_plan* p, double m, double eps, int32_t max_iters, double* v_out,
       a.finalize_local = 1;  // every rank finalizes from the exchanged global root
       a.debug_delay_ns = p->debug_delay_ns;
       a.debug_shared_parts = p->debug_shared_parts;
+      a.peer_timeout_ns = (uint64_t)p->peer_timeout_ms * 1000000ull;
       if (p->profile && i == 0) {
         const int passes = std::min(max_iters, 64);
         if (!p->prof) {
@@ -970,6 +983,7 @@ int fcm_run(fcm_plan* p, double m, double eps, int32_t max_iters, double* v_out,
     if (e == cudaSuccess) {
       p->passes_launched = 1;
       looped = true;
+      p->looped_last = true;
       p->seeded_in_loop = seed_pass ? 1 : 0;
       for (int i = 1; i < p->nshards; ++i) {  // ev_end on shard 0 covers every shard
         CK(cudaSetDevice(p->sh[i].device));
@@ -1066,9 +1080,32 @@ int fcm_run(fcm_plan* p, double m, double eps, int32_t max_iters, double* v_out,
   if (!h.done) return fail(p, FCM_E_STATE, "loop ended without the done flag");
   if (h.dead == -2) return fail(p, FCM_E_STATE, "device loop watchdog fired (internal error)");
   if (h.dead == -3) return fail(p, FCM_E_STATE, "loop kernel grid barrier timed out (internal error)");
+  if (h.dead == -4)
+    return fail(p, FCM_E_NCCL,
+                "rank %d: the pass-%u root of rank %d did not arrive within %lld ms (peer process dead or stuck)",
+                p->nshards > 1 ? 0 : p->rank, h.stuck_pass, h.stuck_rank, (long long)p->peer_timeout_ms);
   if (h.dead >= 0) return fail(p, FCM_E_DEGENERATE, "cluster %d has zero total membership weight", h.dead);
   p->run_ok = true;
   return FCM_OK;
+}
+
+// Single-process multi-shard plans run one loop kernel per shard; shards on
+// the same device rely on those kernels being co-scheduled, which CUDA does
+// not promise (MPS limits, sanitizers, CUDA_LAUNCH_BLOCKING).  If the
+// in-kernel exchange or barrier times out there, the solve is redone with
+// one launch per pass (same tree, same bits).  Multi-process ranks and
+// single-shard plans report the failure instead.
+int fcm_run(fcm_plan* p, double m, double eps, int32_t max_iters, double* v_out,
+            double* trace_out, int32_t* iterations, int32_t* converged, int32_t* dead_cluster) {
+  int rc = run_impl(p, m, eps, max_iters, v_out, trace_out, iterations, converged, dead_cluster);
+  if (rc != FCM_OK && rc != FCM_E_DEGENERATE && rc != FCM_E_ARG && p && p->looped_last && p->nshards > 1 &&
+      p->nranks == p->nshards && p->host_ctl && (p->host_ctl->dead == -3 || p->host_ctl->dead == -4)) {
+    ++p->loop_fallbacks;
+    p->force_per_pass = true;
+    rc = run_impl(p, m, eps, max_iters, v_out, trace_out, iterations, converged, dead_cluster);
+    p->force_per_pass = false;
+  }
+  return rc;
 }
 
 int fcm_download(fcm_plan* p, double* u_out, int32_t* labels_out) {
@@ -1108,6 +1145,7 @@ int fcm_download(fcm_plan* p, double* u_out, int32_t* labels_out) {
     CK(cudaSetDevice(p->sh[i].device));
     CK(cudaStreamSynchronize(p->sh[i].stream));
   }
+  if (labels_out) p->labels_valid = true;
   return FCM_OK;
 }
 
@@ -1200,6 +1238,7 @@ int fcm_download_table(fcm_plan* p, const uint8_t* x_host, double* u_out, int32_
     CK(cudaSetDevice(p->sh[i].device));
     CK(cudaStreamSynchronize(p->sh[i].stream));
   }
+  p->labels_valid = true;  // the full-size epilogue wrote the device labels
   return FCM_OK;
 }
 
@@ -1236,7 +1275,7 @@ int fcm_narrow_pixels(const double* x, int64_t n, int32_t x_kind, void* out, int
 int fcm_last_timing(const fcm_plan* p, double* out, int32_t count) {
   if (!p || !out) return FCM_E_ARG;
   const double v[] = {p->t_loop_ms, p->t_pass_ms, p->t_pro_ms, (double)p->passes_launched,
-                      (double)p->passes_done, (double)p->seeded_in_loop};
+                      (double)p->passes_done, (double)p->seeded_in_loop, (double)p->loop_fallbacks};
   for (int i = 0; i < count && i < (int)(sizeof v / sizeof v[0]); ++i) out[i] = v[i];
   return FCM_OK;
 }
@@ -1258,7 +1297,8 @@ static int label_stats(fcm_plan* p, const int32_t* ref, int32_t cref, const uint
   for (int i = 0; i < p->nshards; ++i) {
     Shard& s = p->sh[i];
     if (s.g.n_local == 0) continue;
-    if (!s.out_labels) return fail(p, FCM_E_STATE, "download the labels (fcm_download) first");
+    if (!s.out_labels || !p->labels_valid)
+      return fail(p, FCM_E_STATE, "download the labels of the last fcm_run (fcm_download / fcm_download_table) first");
     CK(cudaSetDevice(s.device));
     int32_t* dref = nullptr;
     uint8_t* dmask = nullptr;

@@ -47,6 +47,7 @@ struct PassArgs {
   unsigned debug_delay_ns;  // FCM_OPT_DEBUG_DELAY: one CTA per pass sleeps this long after the grid
                             // barrier (race-detection test; 0 in production)
   int debug_shared_parts;   // FCM_OPT_DEBUG_SHARED_PARTIALS: one tile-partial buffer for every pass
+  uint64_t peer_timeout_ns; // loop kernel, multi-rank: wait this long for a peer's root (FCM_OPT_PEER_TIMEOUT_MS)
 };
 constexpr int kProbeSlots = 20;
 

@@ -203,7 +203,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) loop_tma_kernel(PassArgs a) {
     if (tid == 0) probe(a, it, 10, global_ns());
     if (a.mb_ranks > 1 && !exchange_roots(a, rs.root, gen)) {
       if (tid == 0) {
-        a.ctl->dead = -3;
+        a.ctl->dead = -4;  // a peer's root never arrived (ctl->stuck_rank / stuck_pass)
         a.ctl->done = 1;
       }
       break;

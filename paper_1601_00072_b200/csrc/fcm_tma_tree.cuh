@@ -455,7 +455,8 @@ __device__ __forceinline__ void finalize_loop(const PassArgs& a, const double* r
 // the local mailbox, and replace root[] by the rank-ordered pair tree over
 // them -- the same tree the octants use (tree_model.combine_ranks), so the
 // global root is the single-rank root bit for bit.  All threads call it.
-// Returns false on a 4 s timeout (a peer died): the run is flagged.
+// Returns false when a peer's root does not arrive within peer_timeout_ns
+// (a peer died or is stuck): the rank and pass are recorded for the host.
 __device__ __forceinline__ bool exchange_roots(const PassArgs& a, double* root, unsigned gen) {
   const int tid = threadIdx.x;
   const int nf = 2 * a.c + 2;
@@ -474,8 +475,10 @@ __device__ __forceinline__ bool exchange_roots(const PassArgs& a, double* root, 
     for (int r = 0; r < a.mb_ranks && s_ok; ++r)
       while (ld_acquire_sys_u32(&a.mbox_local->tag[par][r]) != tag) {
         __nanosleep(64);
-        if (global_ns() - t0 > 4000000000ull) {
+        if (global_ns() - t0 > a.peer_timeout_ns) {  // rank r is dead or stuck: name it
           s_ok = 0;
+          a.ctl->stuck_rank = r;
+          a.ctl->stuck_pass = gen;
           break;
         }
       }

@@ -277,7 +277,8 @@ class FcmPlan:
         return d
 
     def timing(self) -> dict:
-        keys = ("loop_ms", "pass_ms", "prologue_ms", "passes_launched", "passes", "seeded_in_loop")
+        keys = ("loop_ms", "pass_ms", "prologue_ms", "passes_launched", "passes", "seeded_in_loop",
+                "loop_fallbacks")
         buf = (ctypes.c_double * len(keys))()
         check(lib().fcm_last_timing(self._h, buf, len(keys)), self._h, "fcm_last_timing")
         return dict(zip(keys, list(buf)))

@@ -105,7 +105,8 @@ def match_clusters_gpu(plan, ref: LabelMap, c: int) -> tuple:
     """match_clusters for the labels of `plan`'s last solve, counted on the device."""
     if ref.c > c or plan.c > c:
         raise DimensionMismatchError(f"label maps use more than {c} clusters")
-    conf = plan.confusion(ref.labels, c)
+    conf = np.zeros((c, c), dtype=np.int64)  # rows of clusters the plan does not have stay 0,
+    conf[: plan.c, :] = plan.confusion(ref.labels, c)  # as in the reference's c x c bincount
     return greedy_match(conf)
 
 

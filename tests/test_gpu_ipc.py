@@ -24,3 +24,22 @@ def test_two_process_mailbox_exchange_bitwise():
                        capture_output=True, text=True, timeout=240)
     assert r.returncode == 0, r.stderr[-2000:]
     assert open(out).read().startswith("OK"), open(out).read()
+
+
+@pytest.mark.parametrize("mode", ["--stuck-rank", "--kill-rank"])
+def test_dead_or_stuck_peer_names_the_rank(mode):
+    """A peer that never publishes its per-pass root -- hung (alive, never
+    runs) or crashed (exits after connecting) -- fails the surviving rank's
+    fcm_run with FCM_E_NCCL (DeviceError) naming rank 1 and the pass, after
+    the configured peer timeout (FCM_OPT_PEER_TIMEOUT_MS), instead of a 4 s
+    spin ending in a generic internal error."""
+    out = os.path.join(REPO, "gpurun_out", "ipc_two_ranks.txt")
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    if os.path.exists(out):
+        os.remove(out)
+    r = subprocess.run([sys.executable, os.path.join(REPO, "tools", "ipc_two_ranks.py"), "--same-gpu", mode, "1"],
+                       capture_output=True, text=True, timeout=240)
+    assert r.returncode == 0, r.stderr[-2000:]
+    got = open(out).read()
+    assert got.startswith("OK-FAILED"), got
+    assert "rank 1" in got and "pass" in got

@@ -32,6 +32,18 @@ def test_confusion_and_overlaps_vs_host():
             metrics.match_clusters(res.labels, LabelMap(300_001, 1, ref, 3), 4)
 
 
+def test_match_clusters_gpu_fewer_predicted_clusters():
+    """plan.c < c: the device confusion is plan.c x c; the reference builds a
+    c x c matrix whose extra prediction rows are zero (metrics.py:78-97)."""
+    x = mixture_pixels(100_001, 3, seed=8)
+    res, plan = pkg.run_fcm_gpu(GrayImage(100_001, 1, x), pkg.FcmConfig(c=3, m=2.0, epsilon=1e-5), keep_plan=True)
+    with plan:
+        ref = np.random.default_rng(2).integers(0, 4, size=x.shape[0]).astype(np.int32)
+        want = metrics.match_clusters(res.labels, LabelMap(100_001, 1, ref, 4), 4)
+        got = metrics.match_clusters_gpu(plan, LabelMap(100_001, 1, ref, 4), 4)
+        assert len(got) == 4 and got == want
+
+
 def test_pgm_raster_goes_straight_to_u8(tmp_path):
     x8 = make_config("C1")
     p = tmp_path / "c1.pgm"

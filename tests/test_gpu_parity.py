@@ -446,3 +446,52 @@ def test_late_cta_after_grid_barrier_bitwise(name):
         racy = None
     assert racy is None or racy[2] != base[2] or racy[0].tobytes() != base[0].tobytes() \
         or racy[1].tobytes() != base[1].tobytes() or racy[4].tobytes() != base[4].tobytes()
+
+
+def test_multi_shard_loop_timeout_falls_back_to_per_pass_bitwise():
+    """Shards sharing one GPU run one loop kernel each, which CUDA does not
+    promise to co-schedule.  When the in-kernel exchange times out (forced
+    here with a zero peer timeout) the solve is redone with one launch per
+    pass: same bits, and fcm_last_timing counts the fallback."""
+    from paper_1601_00072_b200 import _lib
+    x = np.clip(np.rint(mixture_pixels(1_000_003, 3, seed=5)), 0, 255).astype(np.uint8)
+
+    def solve(devs, timeout_ms=None):
+        with pkg.FcmPlan(x.shape[0], 3, _lib.FCM_X_U8, devices=devs) as plan:
+            plan.upload_pixels(x)
+            plan.init_membership(11)
+            if timeout_ms is not None:
+                plan.set_option(_lib.FCM_OPT_PEER_TIMEOUT_MS, timeout_ms)
+            out = plan.run(2.0, 1e-5, 200)
+            t = plan.timing()
+            u, lab = plan.download()
+        return out, u, lab, t
+
+    (va, ta, ka, _), ua, la, t1 = solve(None)
+    (vb, tb, kb, _), ub, lb, t2 = solve([0, 0, 0, 0], timeout_ms=0)
+    assert t1["loop_fallbacks"] == 0 and t2["loop_fallbacks"] == 1
+    assert ka == kb and va.tobytes() == vb.tobytes() and ta.tobytes() == tb.tobytes()
+    assert ua.tobytes() == ub.tobytes() and np.array_equal(la, lb)
+
+
+def test_label_statistics_need_this_runs_labels():
+    """fcm_label_confusion / fcm_mask_overlap count the labels a download left
+    on the device; after a new fcm_run (and before its download) they refuse
+    instead of silently counting the previous solve's labels."""
+    from paper_1601_00072_b200 import _lib
+    r = run_case("C1")
+    x = r["x"].astype(np.uint8)
+    ref = np.zeros(x.shape[0], dtype=np.int32)
+    with pkg.FcmPlan(x.shape[0], 3, _lib.FCM_X_U8) as plan:
+        plan.upload_pixels(x)
+        plan.init_membership(0)
+        plan.run(2.0, 1e-5, 500)
+        with pytest.raises(pkg.FcmError):
+            plan.confusion(ref, 1)
+        plan.download(membership=False)
+        assert plan.confusion(ref, 1).sum() == x.shape[0]
+        plan.run(2.0, 1e-5, 500)
+        with pytest.raises(pkg.FcmError):
+            plan.label_counts()
+        plan.download_table(x, membership=False)
+        assert plan.label_counts().sum() == x.shape[0]
