@@ -34,7 +34,9 @@ using SmemRed = SmemRedT<kNFMax>;
 // producer warp never joins.
 template <bool NAMED>
 __device__ __forceinline__ void red_sync() {
-  if (NAMED) asm volatile("bar.sync 1, %0;" ::"n"(kThreads) : "memory");
+  // barrier.sync (not bar.sync == barrier.sync.aligned): threads of a warp may
+  // arrive from different branches (compute-sanitizer synccheck)
+  if (NAMED) asm volatile("barrier.sync 1, %0;" ::"n"(kThreads) : "memory");
   else __syncthreads();
 }
 

@@ -300,10 +300,10 @@ __device__ __forceinline__ void st_u4(float4* p, float4 v, bool keep, uint64_t p
 // producer and consumers wait on it, the reducer warp only arrives (then
 // goes on reducing its level-1 nodes while thread 0 is in the grid barrier).
 __device__ __forceinline__ void bar_sync_end() {
-  asm volatile("bar.sync 2, %0;" ::"n"(kTmaThreads) : "memory");
+  asm volatile("barrier.sync 2, %0;" ::"n"(kTmaThreads) : "memory");  // non-aligned: see red_sync
 }
 __device__ __forceinline__ void bar_arrive_end() {
-  asm volatile("bar.arrive 2, %0;" ::"n"(kTmaThreads) : "memory");
+  asm volatile("barrier.arrive 2, %0;" ::"n"(kTmaThreads) : "memory");
 }
 
 // Orders this thread's generic-proxy view (u_k written by other CTAs, made
