@@ -287,7 +287,7 @@ int setup_shard(fcm_plan* p, Shard& s) {
   if ((rc = dalloc(p, s, &s.u, (size_t)s.g.plane * p->c))) return rc;
   const double resident = (double)s.g.plane * (double)(xsz + 4 * p->c);
   s.keep_l2 = resident <= 0.8 * (double)prop.l2CacheSize ? 1 : 0;
-  if ((rc = dalloc(p, s, &s.tile_part, (size_t)2 * std::max(s.g.tiles_local, 1) * nf))) return rc;
+  if ((rc = dalloc(p, s, &s.tile_part, (size_t)3 * std::max(s.g.tiles_local, 1) * nf))) return rc;
   size_t cnt_total = 0;
   for (int l = 1; l <= s.g.levels; ++l) {
     if ((rc = dalloc(p, s, &s.node_part[l], (size_t)s.g.noct * s.g.nodes[l] * nf))) return rc;
@@ -309,7 +309,7 @@ int setup_shard(fcm_plan* p, Shard& s) {
   CK(cudaMemsetAsync(s.node_cnt[1], 0, sizeof(unsigned) * s.cnt_total, s.stream));
   CK(cudaMemsetAsync(s.ctl, 0, sizeof(Control), s.stream));
   // every tree slot starts unpublished (all-ones NaN pattern, see fcm_kernels.cuh)
-  CK(cudaMemsetAsync(s.tile_part, 0xff, sizeof(double) * 2 * std::max(s.g.tiles_local, 1) * nf, s.stream));
+  CK(cudaMemsetAsync(s.tile_part, 0xff, sizeof(double) * 3 * std::max(s.g.tiles_local, 1) * nf, s.stream));
   for (int l = 1; l <= s.g.levels; ++l)
     CK(cudaMemsetAsync(s.node_part[l], 0xff, sizeof(double) * s.g.noct * s.g.nodes[l] * nf, s.stream));
   return FCM_OK;
@@ -905,7 +905,7 @@ static int run_impl(fcm_plan* p, double m, double eps, int32_t max_iters, double
     CK(cudaMemcpyAsync(s.ctl, p->host_tmpl, sizeof(Control), cudaMemcpyHostToDevice, s.stream));
     CK(cudaMemsetAsync(s.node_cnt[1], 0, sizeof(unsigned) * s.cnt_total, s.stream));
     const int nf = nf_of(p->c);
-    CK(cudaMemsetAsync(s.tile_part, 0xff, sizeof(double) * 2 * std::max(s.g.tiles_local, 1) * nf, s.stream));
+    CK(cudaMemsetAsync(s.tile_part, 0xff, sizeof(double) * 3 * std::max(s.g.tiles_local, 1) * nf, s.stream));
     for (int l = 1; l <= s.g.levels; ++l)
       CK(cudaMemsetAsync(s.node_part[l], 0xff, sizeof(double) * s.g.noct * s.g.nodes[l] * nf, s.stream));
     CK(cudaMemsetAsync(s.l1_buf, 0xff, sizeof(double) * 3 * s.g.noct * s.g.nodes[1] * nf, s.stream));

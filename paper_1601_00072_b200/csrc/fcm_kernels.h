@@ -23,8 +23,8 @@ struct PassArgs {
   int max_iters;
   int seq;                // pass sequence number in this run (tile-scheduler parity)
   Geometry g;
-  double* tile_part;      // level 0: [2][tiles_local][nf] (the loop kernel's small-volume path
-                          // alternates the two halves by pass parity; every other path uses half 0)
+  double* tile_part;      // level 0: [3][tiles_local][nf] (the loop kernel's small-volume path
+                          // rotates the three buffers by pass generation; every other path uses buffer 0)
   double* node_part[kMaxLevels + 1];  // level l >= 1: [noct][nodes[l]][nf]
   unsigned* node_cnt[kMaxLevels + 1]; // level l >= 1: [noct][nodes[l]] arrival counters
   double* rank_root;      // [nf]

@@ -89,16 +89,19 @@ __global__ void __launch_bounds__(kTmaThreads, 2) loop_tma_kernel(PassArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ RedSlots<NF> rs;
   __shared__ double oroot[kOctants][NF];
-  __shared__ double vsh[C];
-  __shared__ double vnew[C];
-  __shared__ double vprev[C];     // recompute mode: centers of the previous pass
+  __shared__ double vsh[C];        // centers at launch (ctl->v)
+  __shared__ double vprev[C];      // recompute mode: centers of the previous pass
   __shared__ double sdelta;       // recompute mode: delta of this pass from the tables
   __shared__ uint32_t spresent[8];
   __shared__ int s_done;
+  __shared__ volatile int s_abort;  // producer: the previous pass's barrier timed out
+  __shared__ unsigned s_gate;       // producer -> reducer: previous pass's barrier seen (generation)
   __shared__ __align__(8) uint64_t upbar;  // bulk copy of the tile partials (small volumes)
   const int tid = threadIdx.x;
   const int c = C <= 8 ? C : a.c;
   if (tid == 0) {
+    s_abort = 0;
+    s_gate = 0u;
     mbar_init(smem_u32(&upbar), 1);
     tma_init_barriers<XT, C, MODE>(smem, rs);
     s_done = *(volatile int*)&a.ctl->done;
@@ -107,8 +110,21 @@ __global__ void __launch_bounds__(kTmaThreads, 2) loop_tma_kernel(PassArgs a) {
   const Powers pw = load_powers(a);
   const int64_t l1_len = (int64_t)a.g.noct * a.g.nodes[1] * (2 * a.c + 2);  // one of 3 buffers
   // small volumes (<= 1024 tiles): no level-1 owners -- every CTA reduces
-  // the level-1 nodes itself after the grid barrier (one hop less per pass)
+  // the level-1 nodes itself after the grid barrier (one hop less per pass),
+  // in one fused step when the geometry fits a warp (loop_root_small)
   const bool from_tiles = a.g.tiles_local <= kSmallTiles;
+  const int fusedP = from_tiles ? fused_lanes_per_octant(a.g) : 0;
+  // fence-free pass end (small volumes whose tree fits one warp, loop_root_small):
+  // tile partials rotate over THREE buffers by pass generation g (buffer
+  // g % 3); the reducer publishing tile t in pass g also resets t's slot in
+  // buffer (g+1) % 3 -- last read in pass g-2, i.e. before every CTA arrived
+  // at the barrier of pass g-1, which the producer has observed first.  Each
+  // CTA arrives at the grid barrier after its stream and immediately polls
+  // the published partials for the root (no wait); the barrier is awaited by
+  // the producer of the next pass, after its static first tile (whose
+  // u_{k-1} this CTA wrote itself), before it claims tiles other CTAs wrote.
+  const bool proto_s = fusedP != 0 && !a.debug_shared_parts;
+  const int64_t tlen = (int64_t)a.g.tiles_local * (2 * a.c + 2);
   // recompute mode (SURVEY 8(d) "effective"): passes >= 2 stream x only;
   // u_{k-1} is never read back -- delta_k = max over the intensities present
   // of |u_k(b) - u_{k-1}(b)| from the two pass tables (fp64, exact)
@@ -117,32 +133,45 @@ __global__ void __launch_bounds__(kTmaThreads, 2) loop_tma_kernel(PassArgs a) {
   if (!from_tiles)
     for (int lo = 0; lo < a.g.noct; ++lo) l1_real += (unsigned)octant_real_nodes(a.g, a.g.oct0 + lo, 1);
   Pipe ps, sp;
-  unsigned gen = 0;  // grid-barrier generations
-  // monotone tile scheduler: every producer makes exactly one failing claim
-  // per pass, so pass p hands out [p(T+G), p(T+G)+T) -- no per-pass reset
-  uint32_t upphase = 0;
-  unsigned sched = 0;
-  const unsigned sched_step = (unsigned)a.g.tiles_local + gridDim.x;
+  // monotone tile scheduler: CTA b starts every pass with tile b (no claim),
+  // the counter hands out tiles G..T-1 and every producer makes exactly one
+  // failing claim, so pass p takes counter values [pT, pT+T) -- no per-pass
+  // reset (grid <= tiles, launch_loop_tma)
+  // (loop-carried counters are derived from `it`, not kept in registers: the
+  // kernel sits at the 96-register cap of 2 CTAs x 320 threads per SM)
+  const unsigned sched_step = (unsigned)a.g.tiles_local;
   __syncthreads();
-  for (unsigned it = a.seed_pass ? 0u : 1u; !s_done && it <= (unsigned)a.max_iters; ++it) {
+  const unsigned it0 = a.seed_pass ? 0u : 1u;
+  for (unsigned it = it0; !s_done && it <= (unsigned)a.max_iters; ++it) {
     if (tid == 0) probe(a, it, 0, global_ns());
     // level-1 results of this pass: buffer (gen+1) % 3; owners publish them
     // after their CTA has entered the grid barrier and count them in
-    // ctl->l1_done (fence + atomic per node); readers wait for the count
-    const unsigned gnext = gen + 1;
+    // ctl->l1_done (release reduction per node); readers wait for the count
+    const unsigned gnext = it - it0 + 1;  // grid-barrier generation closing this pass
+    const unsigned sched = (it - it0) * sched_step;
     double* l1 = a.l1_buf + (gnext % 3) * l1_len;
     // small volumes: this pass's tile partials go to the half of tile_part of
     // its parity.  Every CTA reads them after the grid barrier while early
     // CTAs may already publish the next pass's partials -- into the other
     // half; pass it+2 reuses this half only after the barrier of pass it+1,
     // which no CTA passes before every CTA has finished reading.
-    double* tpart = a.tile_part + (from_tiles && !a.debug_shared_parts
-                                   ? (int64_t)(gnext & 1u) * a.g.tiles_local * (2 * a.c + 2) : 0);
+    // (formed where used: a pointer live across the stream would cost the
+    // consumers a register at the cap)
+    auto tpart_of = [&](unsigned g) {
+      return a.tile_part + (proto_s ? (int64_t)(g % 3u) * tlen
+                            : from_tiles && !a.debug_shared_parts ? (int64_t)(g & 1u) * tlen : 0);
+    };
     if (tid >= kThreads) {
       if (tid == kProducerTid) {
         fence_proxy_async_global();
+        const ProduceGate gate{&a.ctl->bar_count, (gnext - 1u) * gridDim.x, &s_gate, gnext};
         const int n = tma_produce<XT, C, MODE>(a, smem, ps, &a.ctl->tile_next[1], it, it == 0 || (recomp && it >= 2),
-                                                     sched);
+                                                     sched, true, proto_s ? &gate : nullptr);
+        if (n < 0) {
+          a.ctl->dead = -3;  // a stuck CTA (cannot happen with co-resident CTAs): flag the run
+          a.ctl->done = 1;
+          s_abort = 1;
+        }
         probe(a, it, 1, global_ns());
         probe(a, it, 4, (uint64_t)n);
         unsigned smid;
@@ -152,7 +181,8 @@ __global__ void __launch_bounds__(kTmaThreads, 2) loop_tma_kernel(PassArgs a) {
       if ((tid >> 5) == kReducerWarp) {
         // slots first (then arrive at the pass-end barrier), owned level-1
         // nodes after -- overlapping the grid barrier
-        tma_reduce<C, true>(a, rs, sp, &a.ctl->tile_next[1], l1, it, from_tiles, sched, tpart);
+        tma_reduce<C, true>(a, rs, sp, &a.ctl->tile_next[1], l1, it, from_tiles, sched, tpart_of(gnext),
+                            proto_s ? tpart_of(gnext + 1u) : nullptr, &s_gate, gnext);
         if ((tid & 31) == 0) probe(a, it, 7, global_ns());
       } else {
         bar_sync_end();
@@ -161,45 +191,85 @@ __global__ void __launch_bounds__(kTmaThreads, 2) loop_tma_kernel(PassArgs a) {
       if (it == 0) {
         tma_consume_seed<XT, C, MODE>(a, smem, ps, rs, sp, pw);
       } else {
+        // centers of this pass: v_{k} = root[j] / root[c + j] of the previous
+        // pass (the IEEE quotient loop_decide publishes), formed by every
+        // consumer from the shared root -- rs.root is rewritten only after
+        // this pass's grid barrier; the run's first pass takes ctl->v
         double v[C];
 #pragma unroll
-        for (int j = 0; j < C; ++j) v[j] = j < c ? vsh[j] : 0.0;
+        for (int j = 0; j < C; ++j) v[j] = j >= c ? 0.0 : it == it0 ? vsh[j] : rs.root[j] / rs.root[c + j];
         double lwx[C], lwb[C], ljb = 0.0;
         if (LUT) tma_build_lut<C>(smem + L::kLutOff, v, c, pw, lwx, lwb, ljb);
         if (MODE == MODE_LUT2) tma_build_lut2<C>(smem + L::kLutOff, v);
         if (recomp && it >= 2) {
           if (tid < 8) spresent[tid] = __ldcg(&a.ctl->present[tid]);
           red_sync<true>();
-          table_delta<C>(v, vprev, spresent, c, &sdelta);
+          table_delta<C>(v, vprev, spresent, c, &sdelta);  // (vprev: v_{k-1}, stored below last pass)
           tma_consume<XT, C, MODE, true>(a, smem, ps, rs, sp, v, pw, lwx, lwb, ljb, it);
         } else {
           tma_consume<XT, C, MODE>(a, smem, ps, rs, sp, v, pw, lwx, lwb, ljb, it);
+        }
+        if (recomp) {  // read after the next grid barrier (constant indices: v stays in registers)
+#pragma unroll
+          for (int j = 0; j < C; ++j)
+            if (tid == j && j < c) vprev[j] = v[j];
         }
         if (tid == 0) probe(a, it, 2, global_ns());
       }
       bar_sync_end();
     }
-    gen = gnext;
-    sched += sched_step;
-    if (tid == 0) {
-      if (!grid_barrier(a.ctl, gen, gridDim.x) || (l1_real && !wait_count(&a.ctl->l1_done, gen * l1_real))) {
-        a.ctl->dead = -3;  // a stuck CTA (cannot happen with co-resident CTAs): flag the run
-        a.ctl->done = 1;
-        s_done = 1;
+    const unsigned gen = gnext;
+    uint32_t upphase = (it - it0) & 1u;  // bulk copies of the tile partials so far (one per pass)
+    const double* tpart = tpart_of(gnext);
+    if (proto_s) {
+      // arrive (release: this CTA's u_k and tile partials), do not wait
+      if (tid == 0) {
+        red_release_add(&a.ctl->bar_count, 1u);
+        probe(a, it, 3, global_ns());
       }
-      probe(a, it, 3, global_ns());
-    }
-    __syncthreads();
-    if (s_done) break;
-    if (a.debug_delay_ns) {  // race test: one CTA (a different one each pass) reads late
-      if (tid == 0 && blockIdx.x == (it * 7u + 1u) % gridDim.x) {
-        const uint64_t t0 = global_ns();
-        while (global_ns() - t0 < a.debug_delay_ns) __nanosleep(1000);
+      if (a.debug_delay_ns) {  // race test: one CTA (a different one each pass) reads late
+        if (tid == 0 && blockIdx.x == (it * 7u + 1u) % gridDim.x) {
+          const uint64_t t0 = global_ns();
+          while (global_ns() - t0 < a.debug_delay_ns) __nanosleep(1000);
+        }
+        __syncthreads();
+      }
+      const double xdelta = (recomp && it >= 2) ? sdelta : 0.0;
+      const bool ok = loop_root_small<NF>(a, reinterpret_cast<double*>(smem), L::kRingBytes / 8, tpart, fusedP,
+                                          rs.root, it, xdelta, 0u, &upphase, true);
+      if (!ok || s_abort) {
+        if (tid == 0) {
+          a.ctl->dead = -3;
+          a.ctl->done = 1;
+        }
+        break;
+      }
+    } else {
+      if (tid == 0) {
+        if (!grid_barrier(a.ctl, gen, gridDim.x) || (l1_real && !wait_count(&a.ctl->l1_done, gen * l1_real))) {
+          a.ctl->dead = -3;  // a stuck CTA (cannot happen with co-resident CTAs): flag the run
+          a.ctl->done = 1;
+          s_done = 1;
+        }
+        probe(a, it, 3, global_ns());
       }
       __syncthreads();
+      if (s_done) break;
+      if (a.debug_delay_ns) {  // race test: one CTA (a different one each pass) reads late
+        if (tid == 0 && blockIdx.x == (it * 7u + 1u) % gridDim.x) {
+          const uint64_t t0 = global_ns();
+          while (global_ns() - t0 < a.debug_delay_ns) __nanosleep(1000);
+        }
+        __syncthreads();
+      }
+      const double xdelta = (recomp && it >= 2) ? sdelta : 0.0;
+      if (fusedP)
+        loop_root_small<NF>(a, reinterpret_cast<double*>(smem), L::kRingBytes / 8, tpart, fusedP, rs.root, it,
+                            xdelta, smem_u32(&upbar), &upphase);
+      else
+        loop_upper<NF>(a, l1, reinterpret_cast<double*>(smem), oroot, rs.root, it, from_tiles, xdelta,
+                       smem_u32(&upbar), &upphase, L::kRingBytes / 8, tpart);
     }
-    loop_upper<NF>(a, l1, reinterpret_cast<double*>(smem), oroot, rs.root, it, from_tiles,
-                   (recomp && it >= 2) ? sdelta : 0.0, smem_u32(&upbar), &upphase, L::kRingBytes / 8, tpart);
     if (tid == 0) probe(a, it, 10, global_ns());
     if (a.mb_ranks > 1 && !exchange_roots(a, rs.root, gen)) {
       if (tid == 0) {
@@ -208,17 +278,13 @@ __global__ void __launch_bounds__(kTmaThreads, 2) loop_tma_kernel(PassArgs a) {
       }
       break;
     }
-    if (tid < c) vnew[tid] = rs.root[tid] / rs.root[c + tid];  // the c divisions side by side
-    __syncthreads();
-    if (tid == 0) {
-      for (int j = 0; j < c; ++j) vprev[j] = vsh[j];  // the centers this pass used
-      finalize_loop(a, rs.root, it, vsh, vnew, &s_done);
-      probe(a, it, 14, global_ns());
-    }
-    __syncthreads();
+    // stop test and v_{k+1}: every thread from the same root (no barrier);
+    // rs.root is next written after the next grid barrier
+    if (loop_decide(a, rs.root, it)) break;
+    if (tid == 0) probe(a, it, 14, global_ns());
   }
-  // leave the scheduler as the run found it (every claim is behind the last barrier)
-  if (blockIdx.x == 0 && tid == 0) a.ctl->tile_next[1] = 0u;
+  // (the scheduler counter and the barrier count are reset by fcm_run's
+  // control-block upload before the next launch)
 }
 
 template <typename XT, int C, int MODE>

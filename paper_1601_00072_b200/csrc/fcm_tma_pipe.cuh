@@ -312,6 +312,12 @@ __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
+// Device-scope release reduction: publishes everything this thread has
+// written or observed (cumulativity through the preceding CTA barrier), then
+// adds -- one MEMBAR.ALL.GPU + a fire-and-forget REDG, no SC fence.
+__device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ unsigned ld_acquire_sys_u32(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -343,9 +349,36 @@ __device__ __forceinline__ void probe(const PassArgs& a, unsigned it, int k, uin
 // One elected thread: claim tiles from `counter` until the rank's tiles are
 // exhausted, stream every chunk of x and of the c planes of u_{k-1} into the
 // ring, then post the end-of-pass marker.
+// `first_static` (loop kernel): CTA b's first tile of every pass is tile b,
+// the counter hands out tiles G.. -- the pass starts streaming without an
+// atomic round trip on the one counter every producer hits at once.
+// `gate` (loop kernel, small volumes): tile b's u_{k-1} was written by this
+// CTA, so its copies go out at once; before the first claimed tile -- whose
+// u_{k-1} another CTA may have written -- the producer waits for the grid
+// barrier of the previous pass (ctl->bar_count >= gate->target, acquire; 0 =
+// none), then raises gate->flag (release, CTA scope) for the reducer.  The
+// barrier is thereby off the critical path: it completes while the static
+// tile streams.  Returns -1 on a barrier timeout (the run is flagged).
+struct ProduceGate {
+  const unsigned* bar_count;
+  unsigned target;
+  unsigned* flag;  // shared memory
+  unsigned flag_val;
+};
+__device__ __forceinline__ void st_release_cta_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.cta.shared.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire_cta_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.cta.shared.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ bool wait_count(unsigned* ctr, unsigned target);
+
 template <typename XT, int C, int MODE>
 __device__ __forceinline__ int tma_produce(const PassArgs& a, uint8_t* smem, Pipe& ps, unsigned* counter,
-                                           unsigned it = 0, bool x_only = false, unsigned base = 0) {
+                                           unsigned it = 0, bool x_only = false, unsigned base = 0,
+                                           bool first_static = false, const ProduceGate* gate = nullptr) {
   using L = TmaLayout<XT, C, MODE>;
   constexpr int S = L::kStages;
   const uint32_t bar0 = smem_u32(smem + L::kBarOff);
@@ -357,14 +390,24 @@ __device__ __forceinline__ int tma_produce(const PassArgs& a, uint8_t* smem, Pip
   const uint64_t pol = keep ? l2_keep_policy() : 0ull;
   const int ntiles = a.g.tiles_local;
   int claimed = 0;
+  const int off = first_static ? (int)gridDim.x : 0;
+  bool aborted = false;
   for (;;) {
-    const int lt = (int)(atomicAdd(counter, 1u) - base);  // (mod 2^32: a monotone counter)
+    if (gate && claimed == 1) {  // the static tile is out: now the previous pass's barrier
+      if (gate->target && !wait_count(const_cast<unsigned*>(gate->bar_count), gate->target)) aborted = true;
+      fence_proxy_async_global();  // other CTAs' u_{k-1} (acquired above) before the bulk copies
+      st_release_cta_u32(gate->flag, gate->flag_val);
+    }
+    // (mod 2^32: a monotone counter)
+    const int lt = (first_static && claimed == 0) ? (int)blockIdx.x
+                   : aborted                     ? ntiles
+                                                 : (int)(atomicAdd(counter, 1u) - base) + off;
     if (lt >= ntiles) {
       mbar_wait(bar0 + 8u * (S + ps.stage), ps.phase ^ 1u);
       meta[ps.stage].tile = -1;
       mbar_arrive(bar0 + 8u * ps.stage);
       ps.advance<S>();
-      return claimed;
+      return aborted ? -1 : claimed;
     }
     ++claimed;
     if (it) probe(a, it, 5, global_ns());
@@ -597,7 +640,7 @@ __device__ __forceinline__ void tma_consume(const PassArgs& a, uint8_t* smem, Pi
   uint32_t dmax_hi = 0;
   uint32_t* hist = reinterpret_cast<uint32_t*>(smem + L::kLutOff + (LUT ? LL::kHistOff : 0));
   int hpar = 0;  // histogram buffer of the current tile
-  bool first = true;
+  bool first = true, chunk_probed = false;
   if (it && tid == 0) probe(a, it, 13, global_ns());
   for (;;) {
     mbar_wait(bar0 + 8u * ps.stage, ps.phase);
@@ -606,6 +649,7 @@ __device__ __forceinline__ void tma_consume(const PassArgs& a, uint8_t* smem, Pi
     const StageMeta mt = meta[ps.stage];
     const uint8_t* st = smem + ps.stage * L::kStageBytes;
     if (mt.tile < 0) {
+      if (it && tid == 0) probe(a, it, 19, global_ns());
       __syncwarp();
       if ((tid & 31) == 0) mbar_arrive(bar0 + 8u * (S + ps.stage));
       ps.advance<S>();
@@ -698,6 +742,10 @@ __device__ __forceinline__ void tma_consume(const PassArgs& a, uint8_t* smem, Pi
 #pragma unroll
     for (int j = 0; j < C; ++j)
       if (j < c) st_u4(reinterpret_cast<float4*>(a.u_nxt + j * a.g.plane + i0), un[j], keep, pol);
+    if (it && tid == 0 && !chunk_probed) {
+      probe(a, it, 18, global_ns());
+      chunk_probed = true;
+    }
     if (mt.last) {
       if (LUT) {
         // every consumer warp has counted the tile: thread b folds bin b

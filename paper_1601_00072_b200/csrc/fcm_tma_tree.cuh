@@ -107,7 +107,8 @@ template <int C, bool LOOP>
 __device__ __forceinline__ void tma_reduce(const PassArgs& a, RedSlots<2 * C + 2>& rs, Pipe& sp,
                                            const unsigned* counter, double* l1_out, unsigned it = 0,
                                            bool no_owners = false, unsigned base = 0,
-                                           double* tile_out = nullptr) {
+                                           double* tile_out = nullptr, double* tile_reset = nullptr,
+                                           const unsigned* gate_flag = nullptr, unsigned gate_val = 0) {
   constexpr int NF = 2 * C + 2;
   const int lane = threadIdx.x & 31;
   const int nf = 2 * a.c + 2;
@@ -130,7 +131,7 @@ __device__ __forceinline__ void tma_reduce(const PassArgs& a, RedSlots<2 * C + 2
     za = cta0 ? NA : (int)blockIdx.x - 1;
   }
   int zb = 0;
-  bool slots_done = false;
+  bool slots_done = false, reset_ok = false;
   uint64_t n_poll = 0, n_node = 0;
 
   uint32_t backoff = 64;
@@ -145,7 +146,16 @@ __device__ __forceinline__ void tma_reduce(const PassArgs& a, RedSlots<2 * C + 2
                                 : (mbar_wait(smem_u32(&rs.full[sp.stage]), sp.phase), true))) {
       const int t = rs.tile[sp.stage];
       if (t >= 0) {
+        // (loop kernel, small volumes: the slot this tile takes two passes
+        // from now is reset to unpublished -- once the producer has seen the
+        // previous pass's grid barrier, i.e. every CTA has finished reading
+        // the pass that last used it)
+        if (tile_reset && !reset_ok) {
+          while (ld_acquire_cta_u32(gate_flag) != gate_val) __nanosleep(32);
+          reset_ok = true;
+        }
         for (int f = lane; f < nf; f += 32) {  // nf <= 34
+          if (tile_reset) st_relaxed(tile_reset + (int64_t)t * nf + f, sentinel());
           const bool mx = f == nf - 1;
           const double(*w)[NF] = rs.w[sp.stage];
           const double q0 = combine(w[0][f], w[1][f], mx);
@@ -186,16 +196,18 @@ __device__ __forceinline__ void tma_reduce(const PassArgs& a, RedSlots<2 * C + 2
       const int last_lt = (int)((long long)oct * g.M - g.tile0 + last);
       // (loop kernel, after this CTA's slots: the barrier may already have
       // re-armed the scheduler, so poll without the hand-out check)
-      node_hot = (LOOP && slots_done) || (int)(ld_relaxed_u32(counter) - base) > last_lt;
+      // (loop kernel: tiles 0..G-1 are every CTA's static first tile, the
+      // counter hands out G..)
+      node_hot = (LOOP && slots_done) || (int)(ld_relaxed_u32(counter) - base) + (LOOP ? G : 0) > last_lt;
       if (node_hot) {
         ++n_poll;
         double* child0 = l == 1 ? a.tile_part + ((int64_t)oct * g.M - g.tile0 + (int64_t)j * kFan) * nf
                                 : a.node_part[l - 1] + ((int64_t)lo * g.nodes[l - 1] + (int64_t)j * kFan) * nf;
         if (LOOP) {  // publish, then count it (readers wait for the count after the grid barrier)
           advance = try_node<NF, false>(child0, nreal, nf, l1_out + ((int64_t)lo * g.nodes[1] + j) * nf);
-          if (advance && lane == 0) {
-            __threadfence();
-            atomicAdd(&a.ctl->l1_done, 1u);
+          if (advance) {  // (warp-uniform) every lane's sentinel resets, then lane 0's release
+            __syncwarp();
+            if (lane == 0) red_release_add(&a.ctl->l1_done, 1u);
           }
         }
         else
@@ -247,6 +259,41 @@ __device__ __forceinline__ double tree32(const double* p, int64_t stride, int nr
 #pragma unroll
     for (int i = 0; i < 32; i += 2 * s2) v[i] = combine(v[i], v[i + s2], mx);
   return v[0];
+}
+
+// The adjacent-pair tree over 16 published slots (relaxed loads of global
+// memory; children >= nreal count as 0.0), retried until no real child holds
+// the unpublished pattern.  False on a 4 s timeout.
+__device__ __forceinline__ bool poll_tree16(const double* p, int64_t stride, int nreal, bool mx, double* out) {
+  const uint64_t t0 = global_ns();
+  for (;;) {
+    double v[16];
+    bool ok = true;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = i < nreal ? ld_relaxed(p + (int64_t)i * stride) : 0.0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) ok = ok && !(i < nreal && is_sentinel(v[i]));
+    if (ok) {
+#pragma unroll
+      for (int s2 = 1; s2 < 16; s2 <<= 1)
+#pragma unroll
+        for (int i = 0; i < 16; i += 2 * s2) v[i] = combine(v[i], v[i + s2], mx);
+      *out = v[0];
+      return true;
+    }
+    __nanosleep(64);
+    if (global_ns() - t0 > 4000000000ull) return false;
+  }
+}
+
+// tree32 over published slots: the 32-leaf adjacent-pair tree is
+// (children 0..15) + (children 16..31), each half polled as above.
+__device__ __forceinline__ bool poll_tree32(const double* p, int64_t stride, int nreal, bool mx, double* out) {
+  double lo = 0.0, hi = 0.0;
+  if (!poll_tree16(p, stride, nreal < 16 ? nreal : 16, mx, &lo)) return false;
+  if (nreal > 16 && !poll_tree16(p + 16 * stride, stride, nreal - 16, mx, &hi)) return false;
+  *out = combine(lo, hi, mx);
+  return true;
 }
 
 // Loop kernel, after the grid barrier of pass `it`: every CTA reduces the
@@ -344,6 +391,95 @@ __device__ __forceinline__ void loop_upper(const PassArgs& a, const double* l1, 
   __syncthreads();
 }
 
+// Loop kernel, small volumes (<= kSmallTiles tiles), after the grid barrier
+// of pass `it`: the rank root from this pass's tile partials with two CTA
+// barriers.  Step A (every thread, one (level-1 node, field) pair each): the
+// node's 32-leaf tree over the tile partials (tree32), into shared memory.
+// Step B (warp w: fields w, w + 10, ...): lane L is (octant lo = L / P,
+// level-1 node j = L % P), P = nodes[1] rounded up to a power of two; the P
+// lanes of an octant meet in the adjacent-pair shuffle tree (the 32-ary
+// level-2 node: children past the real ones are 0.0, and x + 0.0 == x,
+// max(x, 0.0) == x for these non-negative sums), the octant roots (lanes 0,
+// P, .., 7P; missing octants 0.0) in the 8-leaf pair tree -- exactly
+// loop_upper's association, two barriers instead of four.  Eligible when
+// levels <= 2 and noct * P <= 32 (fused_lanes_per_octant > 0); otherwise the
+// caller uses loop_upper.
+__device__ __forceinline__ int fused_lanes_per_octant(const Geometry& g) {
+  if (g.levels > 2) return 0;
+  int P = 1;
+  while (P < g.nodes[1]) P <<= 1;
+  return g.noct * P <= 32 ? P : 0;
+}
+
+// `poll` (the fence-free protocol of the loop kernel): called right after
+// this CTA's own stream, before any grid barrier -- step A reads the slots
+// with relaxed loads and waits for every real one to be published (the tile
+// partials rotate over three buffers, see loop_tma_kernel).  Returns false on
+// a timeout.
+template <int NF>
+__device__ __forceinline__ bool loop_root_small(const PassArgs& a, double* scratch, int64_t scratch_doubles,
+                                                const double* tp, int P, double* root, unsigned it,
+                                                double extra_delta, uint32_t upbar, uint32_t* upphase,
+                                                bool poll = false) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nf = 2 * a.c + 2;
+  const Geometry& g = a.g;
+  const int n1 = g.nodes[1];
+  if (tid == 0) probe(a, it, 16, global_ns());
+  // the rank's tile partials in one bulk copy (TMA) into the idle ring when
+  // they fit: one request stream per CTA instead of 32 loads per thread
+  const int64_t tdoubles = (int64_t)g.tiles_local * nf;
+  const int64_t tpad = (tdoubles + 15) & ~(int64_t)15;
+  const bool bulk = !poll && upbar != 0u && tdoubles > 0 && tpad + 32 * NF <= scratch_doubles;
+  double* l1s = bulk ? scratch + tpad : scratch;  // [noct * n1][NF]
+  bool ok = true;
+  if (bulk) {
+    if (tid == 0) {
+      fence_proxy_async_global();  // partials: generic stores published by the grid barrier
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive_tx(upbar, (uint32_t)(tdoubles * 8));
+      bulk_g2s(smem_u32(scratch), tp, (uint32_t)(tdoubles * 8), upbar);
+    }
+    mbar_wait(upbar, *upphase);
+    *upphase ^= 1u;
+  }
+  // step A: level-1 nodes (consecutive threads take consecutive fields of a node)
+  for (int pr = tid; pr < g.noct * n1 * nf; pr += kTmaThreads) {
+    const int z = pr / nf, f = pr - z * nf;
+    const int lo = z / n1, j = z - lo * n1;
+    const int oct = g.oct0 + lo;
+    const int nreal = (int64_t)oct * g.M < g.T ? node_real_children(g, oct, 1, j) : 0;
+    const int64_t off = ((int64_t)oct * g.M - g.tile0 + (int64_t)j * kFan) * nf + f;
+    double r = 0.0;
+    if (nreal) {
+      if (poll) ok = ok && poll_tree32(tp + off, nf, nreal, f == nf - 1, &r);
+      else r = bulk ? tree32<false>(scratch + off, nf, nreal, f == nf - 1) : tree32<true>(tp + off, nf, nreal, f == nf - 1);
+    }
+    l1s[(int64_t)z * NF + f] = r;
+  }
+  const bool all_ok = __syncthreads_and(ok);
+  if (tid == 0) probe(a, it, 17, global_ns());
+  if (!all_ok) return false;
+  // step B: level 2 and the rank root, one warp per field, shuffles only
+  const int lo = lane / P, j = lane - lo * P;
+  const bool lane_real = lo < g.noct && j < n1;
+  for (int f = warp; f < nf; f += kTmaThreads / 32) {
+    const bool mx = f == nf - 1;
+    double v = lane_real ? l1s[(int64_t)(lo * n1 + j) * NF + f] : 0.0;
+    for (int s = 1; s < P; s <<= 1) {  // level 2: the octant's level-1 nodes
+      const double o = __shfl_down_sync(0xffffffffu, v, s);
+      if ((lane & (2 * s - 1)) == 0) v = combine(v, o, mx);
+    }
+    for (int s = P; s < 8 * P; s <<= 1) {  // the rank root over the octants
+      const double o = __shfl_down_sync(0xffffffffu, v, s & 31);
+      if ((lane & (2 * s - 1)) == 0 && lane + s < 32) v = combine(v, o, mx);
+    }
+    if (lane == 0) root[f] = mx ? fmax(v, extra_delta) : v;  // recompute mode: the table delta
+  }
+  __syncthreads();
+  return true;
+}
+
 // -------------------------------------------------------- grid barrier ----
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   unsigned v;
@@ -362,9 +498,10 @@ __device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
 // times out after 4 s, flags the run, and lets every CTA leave.
 __device__ __forceinline__ bool grid_barrier(Control* ctl, unsigned gen, unsigned ncta) {
   // release this CTA's writes (tile partials, u), arrive, then wait until the
-  // monotone count reaches gen * ncta -- no last-arriver hop, no reset
-  __threadfence();
-  atomicAdd(&ctl->bar_count, 1u);
+  // monotone count reaches gen * ncta -- no last-arriver hop, no reset.
+  // red.release (MEMBAR.ALL.GPU + REDG) instead of __threadfence + atomicAdd
+  // (MEMBAR.SC.GPU + CCTL.IVALL + ATOMG with a return trip)
+  red_release_add(&ctl->bar_count, 1u);
   const unsigned target = gen * ncta;
   const uint64_t t0 = global_ns();
   while ((int)(ld_acquire_u32(&ctl->bar_count) - target) < 0) {
@@ -390,37 +527,20 @@ __device__ __forceinline__ bool wait_count(unsigned* ctr, unsigned target) {
   return true;
 }
 
-// Loop kernel, thread 0 of every CTA after the redundant root of pass `it`:
-// the same decisions as finalize_body (core.py:120-131: converged, max_iters,
-// DegenerateClusterError(j), else v_{k+1}) on the CTA's own copy; CTA 0 also
-// publishes them to the control block and the trace.
-__device__ __forceinline__ void finalize_loop(const PassArgs& a, const double* root, unsigned it, double* vsh,
-                                              const double* vnew, int* s_done) {
+// Loop kernel, EVERY thread once the root of pass `it` is in root[] (shared
+// memory): the decisions of finalize_body (core.py:120-131: converged,
+// max_iters, DegenerateClusterError(j)) evaluated redundantly -- every thread
+// reads the same root, so all decide alike and no CTA barrier or serial
+// thread-0 step sits between the root and the next pass.  Thread 0 of CTA 0
+// publishes the outcome (control block, objective and delta traces, v_{k+1}
+// = root[j] / root[c + j], the IEEE quotient every thread also forms).
+__device__ __forceinline__ bool loop_decide(const PassArgs& a, const double* root, unsigned it) {
   const int c = a.c;
-  if (it == 0) {  // seeded start: v_1 or DegenerateClusterError (core.py:121-123)
-    int dead = -1;
-    for (int j = 0; j < c; ++j)
-      if (root[c + j] == 0.0) {
-        dead = j;
-        break;
-      }
-    if (dead < 0)
-      for (int j = 0; j < c; ++j) vsh[j] = vnew[j];  // root[j] / root[c + j]
-    *s_done = dead >= 0 ? 1 : 0;
-    if (blockIdx.x == 0) {
-      Control* ctl = a.ctl;
-      for (int f = 0; f < 2 * c + 2; ++f) ctl->root[f] = root[f];
-      ctl->dead = dead;
-      if (dead < 0)
-        for (int j = 0; j < c; ++j) ctl->v[j] = vsh[j];
-      ctl->done = dead >= 0 ? 1 : 0;
-    }
-    return;
+  bool conv = false, done = false;
+  if (it != 0) {  // (it == 0: the seeded start -- v_1 or DegenerateClusterError, core.py:121-123)
+    conv = root[2 * c + 1] < a.eps;
+    done = conv || (int)it >= a.max_iters;
   }
-  const int k = (int)it;
-  const double delta = root[2 * c + 1];
-  const bool conv = delta < a.eps;
-  bool done = conv || k >= a.max_iters;
   int dead = -1;
   if (!done)
     for (int j = 0; j < c; ++j)
@@ -429,25 +549,24 @@ __device__ __forceinline__ void finalize_loop(const PassArgs& a, const double* r
         done = true;
         break;
       }
-  if (!done)
-    for (int j = 0; j < c; ++j) vsh[j] = vnew[j];  // root[j] / root[c + j], computed side by side
-  *s_done = done ? 1 : 0;
-  if (blockIdx.x == 0) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
     Control* ctl = a.ctl;
-    for (int f = 0; f < 2 * c + 2; ++f) {
-      ctl->root[f] = root[f];
-      a.rank_root[f] = root[f];
+    for (int f = 0; f < 2 * c + 2; ++f) ctl->root[f] = root[f];
+    if (it != 0) {
+      const int k = (int)it;
+      for (int f = 0; f < 2 * c + 2; ++f) a.rank_root[f] = root[f];
+      ctl->iter = k;
+      a.trace[k - 1] = root[2 * c];
+      a.trace[a.max_iters + k - 1] = root[2 * c + 1];  // delta trace (second half of the buffer)
+      ctl->delta = root[2 * c + 1];
+      ctl->converged = conv ? 1 : 0;
     }
-    ctl->iter = k;
-    a.trace[k - 1] = root[2 * c];
-    a.trace[a.max_iters + k - 1] = delta;  // delta trace (second half of the buffer)
-    ctl->delta = delta;
-    ctl->converged = conv ? 1 : 0;
     ctl->dead = dead;
     if (!done)
-      for (int j = 0; j < c; ++j) ctl->v[j] = vsh[j];
+      for (int j = 0; j < c; ++j) ctl->v[j] = root[j] / root[c + j];
     ctl->done = done ? 1 : 0;
   }
+  return done;
 }
 
 // Loop kernel, multi-rank: publish this rank's root (in root[], every CTA

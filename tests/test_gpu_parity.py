@@ -406,13 +406,15 @@ def test_run_fcm_gpu_uint8_uses_table_download():
 @pytest.mark.parametrize("name", ["C1", "C2", "C3@200000"])
 def test_late_cta_after_grid_barrier_bitwise(name):
     """Race test for the loop kernel's small-volume path (<= 1024 tiles: every
-    CTA reduces the tile partials itself after the grid barrier).  One CTA per
-    pass (a different one each pass) sleeps 100 us between the barrier and its
-    reads while the others run ahead into the next pass and publish new tile
-    partials.  The partials alternate between two buffers by pass parity, so
-    the late reader still sees its own pass: every result is bit-identical to
-    the undelayed run (the reference's determinism contract,
-    parallel.py:1-11, test_parallel.py:214-264)."""
+    CTA reduces the tile partials itself).  One CTA per pass (a different one
+    each pass) sleeps 100 us between its grid-barrier arrival and its reads
+    of the partials while the others run ahead into the next pass, publish
+    new partials and reset the slots of the pass after.  The partials rotate
+    over three buffers by pass generation and a slot is reset only once the
+    previous pass's barrier shows every reader done with it, so the late
+    reader still sees its own pass: every result is bit-identical to the
+    undelayed run (the reference's determinism contract, parallel.py:1-11,
+    test_parallel.py:214-264)."""
     from paper_1601_00072_b200 import _lib
     from paper_1601_00072_b200.phantom import make_config
     x = make_config(name).reshape(-1).astype(np.uint8)
@@ -432,8 +434,9 @@ def test_late_cta_after_grid_barrier_bitwise(name):
     base = solve(0)
     late = solve(100_000)
     assert late[6]["passes_launched"] == 1  # the loop kernel ran the solve
-    # the injected sleeps really happened: >= 100 us per pass
-    assert late[6]["loop_ms"] - base[6]["loop_ms"] >= 0.05 * base[2]  # (the others overlap the next pass)
+    # the injected sleeps really happened: 100 us per pass, of which the
+    # others overlap up to a pass of their own work (>= 25 us per pass remain)
+    assert late[6]["loop_ms"] - base[6]["loop_ms"] >= 0.025 * base[2]
     assert late[2] == base[2] and late[3] == base[3]
     assert late[0].tobytes() == base[0].tobytes() and late[1].tobytes() == base[1].tobytes()
     assert late[4].tobytes() == base[4].tobytes() and np.array_equal(late[5], base[5])
