@@ -47,7 +47,7 @@ CONFIGS = {
     "C5": ((512, 1024, 1024), 8, 1.5, 1e-5),
     "C5s": ((64, 1024, 1024), 8, 1.5, 1e-5),  # 64-slice slab of C5 (profiling)
 }
-KERNELS = {"tma": 0, "ldg": 1, "lut": 2, "direct": 3}
+KERNELS = {"tma": 0, "lut": 2, "direct": 3}
 BYTES_PER_VOXEL_ITER = {3: 25, 8: 65}  # x (u8) + read u_{k-1} fp32 SoA + write u_k
 
 
@@ -483,9 +483,9 @@ def run_ours(args, rank, world, local_rank, dist):
             "traffic": traffic,
             "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured" else peak_kind,
             "bytes_per_voxel_iter": B,
-            "kernel": ("loop_tma_kernel" if looped else ("pass_kernel" if args.kernel == "ldg" else "pass_tma_kernel"))
+            "kernel": ("loop_tma_kernel" if looped else "pass_tma_kernel")
             + "<uint8_t,%d,%s>" % (c, ("MODE_LUT2" if args.kernel == "tma" else "MODE_M2")
-                                   if m == 2.0 and args.kernel in ("tma", "direct", "ldg")
+                                   if m == 2.0 and args.kernel in ("tma", "direct")
                                    else ("MODE_LUT" if args.kernel in ("tma", "lut") else "MODE_GEN")),
             "timing": ("CUDA events around the persistent loop kernel (one launch = every pass of a solve, grid "
                        "barriers included) on its launching stream, timed region" if looped else
@@ -623,8 +623,8 @@ def main():
     ap.add_argument("--no-loop", action="store_true",
                     help="one launch per pass (CUDA graph with a conditional node) instead of the persistent loop kernel")
     ap.add_argument("--kernel", default="tma", choices=sorted(KERNELS),
-                    help="pass kernel: tma (TMA bulk-copy pipeline, auto math; default), ldg "
-                         "(register-staged LDG/STG), lut (TMA + intensity table), direct (TMA + per-voxel math)")
+                    help="pass kernel: tma (TMA bulk-copy pipeline, auto math; default), "
+                         "lut (TMA + intensity table), direct (TMA + per-voxel math)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3

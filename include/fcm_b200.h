@@ -56,7 +56,8 @@ typedef enum {
   FCM_OPT_GRID = 3,    /* force CTAs per pass launch (0 = occupancy-derived, default) */
   FCM_OPT_KERNEL = 4,  /* pass kernel: 0 = TMA bulk-copy pipeline, automatic per-voxel math (default:
                           product form for m == 2, per-pass intensity table for other m on uint8),
-                          1 = register-staged LDG/STG, 2 = TMA + intensity table for every m (uint8),
+                          1 = register-staged LDG/STG (the kernel of 17 <= c <= 32; FCM_E_ARG for c <= 16,
+                          where it lost its A/B and is not built), 2 = TMA + intensity table for every m (uint8),
                           3 = TMA + per-voxel math for every m */
   FCM_OPT_GRAPH = 5,   /* 1 (default): when the loop kernel is off, single-shard runs launch
                           prologue + a device-side while loop (CUDA graph conditional node);
@@ -241,6 +242,11 @@ int fcm_objective(const double* x, const double* u, const double* v, int64_t n, 
                   double m, int32_t device, double* out);
 int fcm_max_abs_diff(const double* a, const double* b, int64_t count, int32_t device, double* out);
 int fcm_argmax_rows(const double* u, int32_t* labels_out, int64_t n, int32_t c, int32_t device);
+
+/* Diagnostics (no reference counterpart): the seeded start's branch-free
+ * correctly rounded reciprocal against CUDA's __drcp_rn on n pseudo-random
+ * row totals in [2^-53, 64); *mismatches = how many differ (expected 0). */
+int fcm_check_rcp(int64_t n, uint64_t seed, int32_t device, int64_t* mismatches);
 
 #ifdef __cplusplus
 }

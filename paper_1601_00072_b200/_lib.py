@@ -68,6 +68,7 @@ SIGNATURES = {
                        ctypes.c_double, ctypes.c_int32, ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
     "fcm_max_abs_diff": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32,
                           ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
+    "fcm_check_rcp": ([ctypes.c_int64, ctypes.c_uint64, ctypes.c_int32, ctypes.c_void_p], ctypes.c_int),
     "fcm_argmax_rows": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32],
                         ctypes.c_int),
 }

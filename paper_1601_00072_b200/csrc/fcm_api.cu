@@ -805,6 +805,8 @@ int fcm_set_option(fcm_plan* p, int32_t key, int64_t value) {
       return FCM_OK;
     case FCM_OPT_KERNEL:
       if (value < 0 || value > 3) return FCM_E_ARG;
+      if (value == 1 && p->c <= 16)  // the register-staged kernel is built for 17 <= c <= 32 only
+        return fail(p, FCM_E_ARG, "FCM_OPT_KERNEL = 1 (register-staged pass kernel) needs c > 16");
       p->variant = (int)value;
       return FCM_OK;
     default: return FCM_E_ARG;
@@ -893,6 +895,7 @@ static int run_impl(fcm_plan* p, double m, double eps, int32_t max_iters, double
   Control tmpl;
   memset(&tmpl, 0, sizeof tmpl);
   tmpl.dead = -1;
+  tmpl.stuck_rank = 0x7fffffff;  // lowest rank whose root never arrived (atomicMin)
   *p->host_tmpl = tmpl;
   for (int i = 0; i < p->nshards; ++i) {
     Shard& s = p->sh[i];
@@ -1557,6 +1560,19 @@ int fcm_max_abs_diff(const double* a, const double* b, int64_t count, int32_t de
   CKS(op_reduce(1, nullptr, nullptr, nullptr, count, 0, 0.0, (double*)da.p, (double*)db.p, s,
                 s + kOpsScratch, 0));
   CKS(cudaMemcpy(out, s + kOpsScratch, sizeof(double), cudaMemcpyDeviceToHost));
+  return FCM_OK;
+}
+
+int fcm_check_rcp(int64_t n, uint64_t seed, int32_t device, int64_t* mismatches) {
+  if (n < 0 || !mismatches) return FCM_E_ARG;
+  CKS(cudaSetDevice(device));
+  DevBuf d;
+  CKS(cudaMalloc(&d.p, sizeof(unsigned long long)));
+  CKS(cudaMemset(d.p, 0, sizeof(unsigned long long)));
+  CKS(op_rcp_check(n, seed, (unsigned long long*)d.p, 0));
+  unsigned long long h = 0;
+  CKS(cudaMemcpy(&h, d.p, sizeof h, cudaMemcpyDeviceToHost));
+  *mismatches = (int64_t)h;
   return FCM_OK;
 }
 

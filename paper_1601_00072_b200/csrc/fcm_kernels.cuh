@@ -117,11 +117,7 @@ __device__ __forceinline__ bool pass_done(const PassArgs& a, SM& sm) {
 // arrivals' stores visible.  Replaces a full __threadfence on every thread.
 __device__ __forceinline__ unsigned atom_add_acq_rel(unsigned* p, unsigned v) {
   unsigned old;
-#ifdef FCM_EXPERIMENT_RELAXED
-  asm volatile("atom.add.relaxed.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
-#else
   asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
-#endif
   return old;
 }
 
@@ -408,11 +404,12 @@ template <int C, int MODE>
 __device__ __forceinline__ void seed_quad(const PassArgs& a, const Powers& pw, int c, int64_t i0,
                                           const double* xd, int64_t nvalid, float4* un, double* acc) {
   constexpr int PM = (MODE == MODE_M2 || MODE == MODE_LUT2) ? MODE_M2 : MODE_GEN;
-  const uint64_t row_step = (uint64_t)c * kGamma;  // SplitMix64 state advance per voxel
+  // SplitMix64 state before voxel i0's first draw; each row advances it by c*GAMMA
+  uint64_t st = a.seed + (uint64_t)(a.g.voxel0 + i0) * ((uint64_t)c * kGamma);
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     double u[C];
-    init_row_state<C>(a.seed + (uint64_t)(a.g.voxel0 + i0 + q) * row_step, c, u);
+    init_row_advance<C>(st, c, u);
     const bool valid = q < nvalid;
 #pragma unroll
     for (int j = 0; j < C; ++j) {
@@ -539,6 +536,9 @@ inline int occupancy_grid(KernelPtr k, int tiles, int sms) {
 // Per-voxel math of a plan: m == 2 product form (C <= 8) or the general
 // robust form.  C == 32 (17 <= c <= 32) runs the register-staged pass kernel
 // only: no shared-memory stage holds 17..32 membership planes of a chunk.
+// For C <= 16 that kernel lost its A/B against the TMA pipeline (round 1:
+// 0.60-0.66 vs 0.51 ms per C4 pass) and is not instantiated (the plan
+// rejects FCM_OPT_KERNEL = 1 there).
 template <int C>
 cudaError_t launch_pass_c(int xkind, int mode, const PassArgs& a, int sms, cudaStream_t st,
                           int* grid_out, int variant, int force_grid) {
@@ -563,7 +563,10 @@ cudaError_t launch_pass_c(int xkind, int mode, const PassArgs& a, int sms, cudaS
                 : launch_pass_tma<double, C, MODE_GEN>(a, sms, st, grid_out, force_grid);
     }
   }
-  int grid = 0;  // variant 1 / C == 32: register-staged LDG/STG kernel
+  if constexpr (C <= 16) {
+    return cudaErrorNotSupported;  // variant 1 (register-staged) is built for C == 32 only
+  } else {
+  int grid = 0;  // C == 32: register-staged LDG/STG kernel
   auto go = [&](auto k) {
     grid = force_grid > 0 ? std::min(force_grid, a.g.tiles_local) : occupancy_grid(k, a.g.tiles_local, sms);
     k<<<grid, kThreads, 0, st>>>(a);
@@ -580,6 +583,7 @@ cudaError_t launch_pass_c(int xkind, int mode, const PassArgs& a, int sms, cudaS
   }
   if (grid_out) *grid_out = grid;
   return cudaGetLastError();
+  }
 }
 
 template <int C>

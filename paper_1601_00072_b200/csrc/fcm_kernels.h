@@ -49,7 +49,7 @@ struct PassArgs {
   int debug_shared_parts;   // FCM_OPT_DEBUG_SHARED_PARTIALS: one tile-partial buffer for every pass
   uint64_t peer_timeout_ns; // loop kernel, multi-rank: wait this long for a peer's root (FCM_OPT_PEER_TIMEOUT_MS)
 };
-constexpr int kProbeSlots = 20;
+constexpr int kProbeSlots = 24;
 
 struct FinalizeArgs {
   const double* roots[kOctants];  // rank r's reduction root (peer, local or NCCL-gathered)

@@ -88,6 +88,29 @@ __global__ void argmax_kernel(const double* u, int32_t* labels, int64_t n, int c
   }
 }
 
+// Diagnostics: drcp_rn_normal (the seeded init's branch-free reciprocal) vs
+// CUDA's __drcp_rn on n SplitMix64-drawn b = 2^e * (1 + f), e uniform in
+// [-53, 5], f uniform in [0, 1) -- the row totals' range.  Counts mismatches.
+__global__ void rcp_check_kernel(int64_t n, uint64_t seed, unsigned long long* bad) {
+  unsigned long long nb = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t z = seed + (uint64_t)(i + 1) * kGamma;
+    z = (z ^ (z >> 30)) * kMix1;
+    z = (z ^ (z >> 27)) * kMix2;
+    z ^= z >> 31;
+    const int e = (int)((z >> 52) % 59u) - 53;
+    const double b = __hiloint2double((int)(((uint32_t)(e + 1023) << 20) | ((uint32_t)(z >> 32) & 0xfffffu)),
+                                      (int)(uint32_t)z);
+    if (__double_as_longlong(drcp_rn_normal(b)) != __double_as_longlong(__drcp_rn(b))) ++nb;
+  }
+  if (nb) atomicAdd(bad, nb);
+}
+
+cudaError_t op_rcp_check(int64_t n, uint64_t seed, unsigned long long* bad, cudaStream_t st) {
+  rcp_check_kernel<<<148 * 8, kThreads, 0, st>>>(n, seed, bad);
+  return cudaGetLastError();
+}
+
 static int grid_for(int64_t n) {
   int64_t g = (n + kThreads - 1) / kThreads;
   if (g > 148 * 16) g = 148 * 16;

@@ -15,4 +15,6 @@ cudaError_t op_argmax(const double* u, int32_t* labels, int64_t n, int c, cudaSt
 // bins[p] += |pred==p & mask|, bins[c] += |mask|, bins[c+1+p] += |pred==p| when mask is set.
 cudaError_t op_label_counts(const int32_t* pred, const int32_t* ref, const uint8_t* mask, int64_t n, int c,
                             int cref, unsigned long long* bins, cudaStream_t st);
+// Diagnostics: mismatches of the seeded init's branch-free reciprocal against __drcp_rn.
+cudaError_t op_rcp_check(int64_t n, uint64_t seed, unsigned long long* bad, cudaStream_t st);
 }  // namespace fcm

@@ -95,13 +95,13 @@ __global__ void __launch_bounds__(kTmaThreads, 2) loop_tma_kernel(PassArgs a) {
   __shared__ uint32_t spresent[8];
   __shared__ int s_done;
   __shared__ volatile int s_abort;  // producer: the previous pass's barrier timed out
-  __shared__ unsigned s_gate;       // producer -> reducer: previous pass's barrier seen (generation)
-  __shared__ __align__(8) uint64_t upbar;  // bulk copy of the tile partials (small volumes)
+  __shared__ __align__(8) uint64_t gatebar;  // producer -> reducer: previous pass's barrier seen
+  __shared__ __align__(8) uint64_t upbar;    // bulk copy of the tile partials (small volumes)
   const int tid = threadIdx.x;
   const int c = C <= 8 ? C : a.c;
   if (tid == 0) {
     s_abort = 0;
-    s_gate = 0u;
+    mbar_init(smem_u32(&gatebar), 1);  // (tma_init_barriers' fence publishes both)
     mbar_init(smem_u32(&upbar), 1);
     tma_init_barriers<XT, C, MODE>(smem, rs);
     s_done = *(volatile int*)&a.ctl->done;
@@ -164,7 +164,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) loop_tma_kernel(PassArgs a) {
     if (tid >= kThreads) {
       if (tid == kProducerTid) {
         fence_proxy_async_global();
-        const ProduceGate gate{&a.ctl->bar_count, (gnext - 1u) * gridDim.x, &s_gate, gnext};
+        const ProduceGate gate{&a.ctl->bar_count, (gnext - 1u) * gridDim.x, smem_u32(&gatebar)};
         const int n = tma_produce<XT, C, MODE>(a, smem, ps, &a.ctl->tile_next[1], it, it == 0 || (recomp && it >= 2),
                                                      sched, true, proto_s ? &gate : nullptr);
         if (n < 0) {
@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) loop_tma_kernel(PassArgs a) {
         // slots first (then arrive at the pass-end barrier), owned level-1
         // nodes after -- overlapping the grid barrier
         tma_reduce<C, true>(a, rs, sp, &a.ctl->tile_next[1], l1, it, from_tiles, sched, tpart_of(gnext),
-                            proto_s ? tpart_of(gnext + 1u) : nullptr, &s_gate, gnext);
+                            proto_s ? tpart_of(gnext + 1u) : nullptr, smem_u32(&gatebar), (gnext - 1u) & 1u);
         if ((tid & 31) == 0) probe(a, it, 7, global_ns());
       } else {
         bar_sync_end();

@@ -356,23 +356,15 @@ __device__ __forceinline__ void probe(const PassArgs& a, unsigned it, int k, uin
 // CTA, so its copies go out at once; before the first claimed tile -- whose
 // u_{k-1} another CTA may have written -- the producer waits for the grid
 // barrier of the previous pass (ctl->bar_count >= gate->target, acquire; 0 =
-// none), then raises gate->flag (release, CTA scope) for the reducer.  The
-// barrier is thereby off the critical path: it completes while the static
-// tile streams.  Returns -1 on a barrier timeout (the run is flagged).
+// none), then arrives on the CTA's gate mbarrier (one phase per pass) for the
+// reducer.  The barrier is thereby off the critical path: it completes while
+// the static tile streams.  Returns -1 on a barrier timeout (the run is
+// flagged).
 struct ProduceGate {
   const unsigned* bar_count;
   unsigned target;
-  unsigned* flag;  // shared memory
-  unsigned flag_val;
+  uint32_t mbar;  // shared-memory mbarrier, count 1
 };
-__device__ __forceinline__ void st_release_cta_u32(unsigned* p, unsigned v) {
-  asm volatile("st.release.cta.shared.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
-}
-__device__ __forceinline__ unsigned ld_acquire_cta_u32(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.cta.shared.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
-  return v;
-}
 __device__ __forceinline__ bool wait_count(unsigned* ctr, unsigned target);
 
 template <typename XT, int C, int MODE>
@@ -396,7 +388,7 @@ __device__ __forceinline__ int tma_produce(const PassArgs& a, uint8_t* smem, Pip
     if (gate && claimed == 1) {  // the static tile is out: now the previous pass's barrier
       if (gate->target && !wait_count(const_cast<unsigned*>(gate->bar_count), gate->target)) aborted = true;
       fence_proxy_async_global();  // other CTAs' u_{k-1} (acquired above) before the bulk copies
-      st_release_cta_u32(gate->flag, gate->flag_val);
+      mbar_arrive(gate->mbar);     // (release, CTA scope) -> the reducer may reset slots
     }
     // (mod 2^32: a monotone counter)
     const int lt = (first_static && claimed == 0) ? (int)blockIdx.x
@@ -640,7 +632,7 @@ __device__ __forceinline__ void tma_consume(const PassArgs& a, uint8_t* smem, Pi
   uint32_t dmax_hi = 0;
   uint32_t* hist = reinterpret_cast<uint32_t*>(smem + L::kLutOff + (LUT ? LL::kHistOff : 0));
   int hpar = 0;  // histogram buffer of the current tile
-  bool first = true, chunk_probed = false;
+  bool first = true;
   if (it && tid == 0) probe(a, it, 13, global_ns());
   for (;;) {
     mbar_wait(bar0 + 8u * ps.stage, ps.phase);
@@ -664,10 +656,11 @@ __device__ __forceinline__ void tma_consume(const PassArgs& a, uint8_t* smem, Pi
     const int64_t i0 = (int64_t)mt.tile * tile + (int64_t)mt.chunk * kChunk + tid * kVec;
     const int64_t nleft = a.g.n_local - i0;
     double xd[4];
+    uint32_t xw = 0;  // uint8: the 4 intensities, also the table rows (no fp64 -> int conversion)
     if (sizeof(XT) == 1) {
-      const uint32_t w = *reinterpret_cast<const uint32_t*>(st + tid * 4);
+      xw = *reinterpret_cast<const uint32_t*>(st + tid * 4);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) xd[q] = u8_to_f64((w >> (8 * q)) & 0xffu);
+      for (int q = 0; q < 4; ++q) xd[q] = u8_to_f64((xw >> (8 * q)) & 0xffu);
     } else if (sizeof(XT) == 2) {
       const uint2 w = *reinterpret_cast<const uint2*>(st + tid * 8);
       xd[0] = u8_to_f64(w.x & 0xffffu);  // (exact for any 32-bit unsigned value)
@@ -699,12 +692,13 @@ __device__ __forceinline__ void tma_consume(const PassArgs& a, uint8_t* smem, Pi
       for (int j = 0; j < C; ++j) uq[j] = f4get(uo[j], q);
       const bool valid = q < nleft;
       if (LUT) {
-        const int b = (int)(xd[q] - 0.0);
+        const int b = (int)((xw >> (8 * q)) & 0xffu);
+        const int br = b;
         float ufv[4 * LL::K4], duv[4 * LL::K4];
 #pragma unroll
         for (int k = 0; k < LL::K4; ++k) {
-          const float4 f = reinterpret_cast<const float4*>(lut + LL::kUfOff)[k * 256 + b];
-          const float4 e = reinterpret_cast<const float4*>(lut + LL::kDuOff)[k * 256 + b];
+          const float4 f = reinterpret_cast<const float4*>(lut + LL::kUfOff)[k * 256 + br];
+          const float4 e = reinterpret_cast<const float4*>(lut + LL::kDuOff)[k * 256 + br];
           ufv[4 * k] = f.x; ufv[4 * k + 1] = f.y; ufv[4 * k + 2] = f.z; ufv[4 * k + 3] = f.w;
           duv[4 * k] = e.x; duv[4 * k + 1] = e.y; duv[4 * k + 2] = e.z; duv[4 * k + 3] = e.w;
         }
@@ -717,12 +711,12 @@ __device__ __forceinline__ void tma_consume(const PassArgs& a, uint8_t* smem, Pi
           nq[j] = ufv[j];
         }
       } else if (LUT2) {
-        const int b = (int)(xd[q] - 0.0);
+        const int br = (int)((xw >> (8 * q)) & 0xffu);
         constexpr int K2 = Lut2Layout<C>::K2;
         double e[2 * K2];
 #pragma unroll
         for (int k = 0; k < K2; ++k) {
-          const double2 w2 = reinterpret_cast<const double2*>(lut)[k * 256 + b];
+          const double2 w2 = reinterpret_cast<const double2*>(lut)[k * 256 + br];
           e[2 * k] = w2.x;
           e[2 * k + 1] = w2.y;
         }
@@ -742,10 +736,6 @@ __device__ __forceinline__ void tma_consume(const PassArgs& a, uint8_t* smem, Pi
 #pragma unroll
     for (int j = 0; j < C; ++j)
       if (j < c) st_u4(reinterpret_cast<float4*>(a.u_nxt + j * a.g.plane + i0), un[j], keep, pol);
-    if (it && tid == 0 && !chunk_probed) {
-      probe(a, it, 18, global_ns());
-      chunk_probed = true;
-    }
     if (mt.last) {
       if (LUT) {
         // every consumer warp has counted the tile: thread b folds bin b

@@ -108,7 +108,7 @@ __device__ __forceinline__ void tma_reduce(const PassArgs& a, RedSlots<2 * C + 2
                                            const unsigned* counter, double* l1_out, unsigned it = 0,
                                            bool no_owners = false, unsigned base = 0,
                                            double* tile_out = nullptr, double* tile_reset = nullptr,
-                                           const unsigned* gate_flag = nullptr, unsigned gate_val = 0) {
+                                           uint32_t gate_mbar = 0u, uint32_t gate_parity = 0u) {
   constexpr int NF = 2 * C + 2;
   const int lane = threadIdx.x & 31;
   const int nf = 2 * a.c + 2;
@@ -151,7 +151,7 @@ __device__ __forceinline__ void tma_reduce(const PassArgs& a, RedSlots<2 * C + 2
         // previous pass's grid barrier, i.e. every CTA has finished reading
         // the pass that last used it)
         if (tile_reset && !reset_ok) {
-          while (ld_acquire_cta_u32(gate_flag) != gate_val) __nanosleep(32);
+          mbar_wait(gate_mbar, gate_parity);  // this pass's phase of the producer's gate
           reset_ok = true;
         }
         for (int f = lane; f < nf; f += 32) {  // nf <= 34
@@ -584,26 +584,38 @@ __device__ __forceinline__ bool exchange_roots(const PassArgs& a, double* root, 
   if (blockIdx.x == 0 && tid < a.mb_ranks) {  // thread p writes rank p's copy (NVLink stores)
     Mailbox* mb = a.mbox_peer[tid];
     for (int f = 0; f < nf; ++f) mb->root[par][a.mb_rank][f] = root[f];
-    __threadfence_system();
+    // (timeline runs: the publication time rides in the slot's unused last
+    // field, so the receiver can time the exchange -- one device, one clock)
+    if (a.prof) mb->root[par][a.mb_rank][kNFMax - 1] = __longlong_as_double((long long)global_ns());
+    // the release orders this thread's own root stores before the tag: no
+    // separate system fence
     st_release_sys_u32(&mb->tag[par][a.mb_rank], tag);
   }
-  __shared__ int s_ok;
-  if (tid == 0) {
-    s_ok = 1;
+  // every rank's tag polled at once (thread r waits for rank r): one
+  // round trip after the last publication, not one per rank
+  bool ok = true;
+  if (tid < a.mb_ranks) {
     const uint64_t t0 = global_ns();
-    for (int r = 0; r < a.mb_ranks && s_ok; ++r)
-      while (ld_acquire_sys_u32(&a.mbox_local->tag[par][r]) != tag) {
-        __nanosleep(64);
-        if (global_ns() - t0 > a.peer_timeout_ns) {  // rank r is dead or stuck: name it
-          s_ok = 0;
-          a.ctl->stuck_rank = r;
-          a.ctl->stuck_pass = gen;
-          break;
-        }
+    while (ld_acquire_sys_u32(&a.mbox_local->tag[par][tid]) != tag) {
+      __nanosleep(32);
+      if (global_ns() - t0 > a.peer_timeout_ns) {  // rank tid is dead or stuck: name it
+        ok = false;
+        atomicMin(&a.ctl->stuck_rank, tid);  // (the lowest missing rank is named)
+        a.ctl->stuck_pass = gen;
+        break;
       }
+    }
   }
-  __syncthreads();
-  if (!s_ok) return false;
+  const bool all_ok = __syncthreads_and(ok) != 0;
+  if (a.prof && all_ok && tid == 0) {  // 21: every root here; 22: the last rank's publication
+    const uint64_t t_all = global_ns();
+    uint64_t t_pub = 0;
+    for (int r = 0; r < a.mb_ranks; ++r)
+      t_pub = max(t_pub, (uint64_t)__double_as_longlong(ld_relaxed_sys(&a.mbox_local->root[par][r][kNFMax - 1])));
+    probe(a, gen - (a.seed_pass ? 1u : 0u), 21, t_all);
+    probe(a, gen - (a.seed_pass ? 1u : 0u), 22, t_pub);
+  }
+  if (!all_ok) return false;
   for (int f = tid; f < nf; f += kTmaThreads) {
     double v[8];
 #pragma unroll

@@ -232,8 +232,10 @@ class FcmPlan:
 
     def profile(self) -> np.ndarray:
         """Loop-kernel timeline of the last run (FCM_OPT_PROFILE): array [pass, cta, slot]
-        with slots 0 start, 1 claims done, 2 consumers done, 3 barrier released (ns), 4 tiles."""
-        slots = 20  # kProbeSlots (fcm_kernels.h)
+        with slots 0 start, 1 claims done, 2 consumers done, 3 barrier arrival (ns), 4 tiles, ...
+        21 / 22 multi-shard root exchange: all roots here / last rank's publication
+        (tools/pass_phases.py, tools/exchange_latency.py)."""
+        slots = 24  # kProbeSlots (fcm_kernels.h)
         cap = 64 * 8 * 1024 * slots
         buf = np.zeros(cap, dtype=np.uint64)
         passes, grid = ctypes.c_int32(), ctypes.c_int32()

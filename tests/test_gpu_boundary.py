@@ -202,3 +202,15 @@ def test_reference_run_benchmark_times_gpu_engine(tmp_path):
     out = tmp_path / "bench.csv"
     bench.write_csv(records, out)
     assert sum(1 for line in out.read_text().splitlines() if ",gpu," in line) == 4
+
+
+def test_register_staged_kernel_only_above_16_clusters():
+    """FCM_OPT_KERNEL = 1 (register-staged pass kernel) is the kernel of
+    17 <= c <= 32 only: it lost its A/B against the TMA pipeline for c <= 16
+    and is not built there, so a c <= 16 plan rejects it by name."""
+    from paper_1601_00072_b200 import _lib
+    with pkg.FcmPlan(10_000, 3, _lib.FCM_X_U8) as plan:
+        with pytest.raises(pkg.InvalidConfigError, match="c > 16"):
+            plan.set_option(_lib.FCM_OPT_KERNEL, 1)
+    with pkg.FcmPlan(10_000, 20, _lib.FCM_X_U8) as plan:
+        plan.set_option(_lib.FCM_OPT_KERNEL, 1)

@@ -86,3 +86,41 @@ def test_init_membership_large_bitwise(n, c, seed):
     got = pkg.init_membership(n, pkg.FcmConfig(c=c, seed=s)).u
     ref = O.fill_membership_random(n, c, seed)
     assert got.tobytes() == ref.tobytes()
+
+
+def test_branch_free_reciprocal_matches_drcp_rn():
+    """The seeded start forms each row's IEEE quotients from one correctly
+    rounded reciprocal of the row total; the loop kernel's copy is CUDA's
+    __drcp_rn fast path without the range test and slow-path call (so four
+    rows interleave).  2^31 pseudo-random totals over the whole range a row
+    total can take ([2^-53, 64)): bit-identical to __drcp_rn."""
+    import ctypes
+    from paper_1601_00072_b200 import _lib
+    bad = ctypes.c_int64(-1)
+    assert _lib.lib().fcm_check_rcp(1 << 31, 0x5EED, 0, ctypes.byref(bad)) == 0
+    assert bad.value == 0
+
+
+def test_seeded_pass_equals_uploaded_reference_rows():
+    """The loop kernel's pass 0 (strength-reduced SplitMix64 state, branch-free
+    reciprocal) against the same solve started from the reference
+    generator's rows uploaded as fp64 (prologue kernel, same tree): 4M voxels,
+    c = 3 and 5, three passes -- centers, objective and delta traces
+    identical bit for bit, so every u_0 row was."""
+    from oracle import oracle as O
+    from paper_1601_00072_b200 import _lib
+    rng = np.random.default_rng(7)
+    n = 4_000_037
+    x = rng.integers(0, 256, n).astype(np.uint8)
+    for c in (3, 5):
+        with pkg.FcmPlan(n, c, _lib.FCM_X_U8) as plan:
+            plan.upload_pixels(x)
+            plan.init_membership(12345)
+            v, trace, k, conv = plan.run(2.0, 1e-300, 3)
+            assert plan.timing()["passes_launched"] == 1  # one loop-kernel launch, seeded in pass 0
+        with pkg.FcmPlan(n, c, _lib.FCM_X_U8) as plan:
+            plan.upload_pixels(x)
+            plan.upload_membership(O.fill_membership_random(n, c, 12345))
+            v2, trace2, k2, conv2 = plan.run(2.0, 1e-300, 3)
+        assert k == k2 == 3
+        assert v.tobytes() == v2.tobytes() and trace.tobytes() == trace2.tobytes()

@@ -5,7 +5,7 @@ pass start (the earliest CTA's), averaged over passes 2..k-1.
     python tools/pass_phases.py C1 C3@1000000 C2 [--warm 20]
 
 Probes (fcm_tma_*.cuh): 0 pass start, 13 consumers enter the stream (LUT
-built), 12 first stage ready, 18 first chunk stored, 19 end-of-pass marker seen, 2 consumers done, 15 reducer drained its slots,
+built), 12 first stage ready, 19 end-of-pass marker seen, 2 consumers done, 15 reducer drained its slots,
 1 producer done claiming, 3 grid barrier released, 16 upper levels start,
 17 level 1 from the tile partials done, 10 upper levels done, 14 finalize done.
 """
@@ -24,7 +24,7 @@ warm = 20
 if "--warm" in sys.argv:
     warm = int(sys.argv[sys.argv.index("--warm") + 1])
     args.remove(str(warm))
-PROBES = [(0, "start"), (13, "lut built"), (12, "1st stage"), (18, "1st chunk stored"), (19, "end marker seen"),
+PROBES = [(0, "start"), (13, "lut built"), (12, "1st stage"), (19, "end marker seen"),
           (2, "consumers done"), (15, "reducer done"),
           (1, "producer done"), (3, "barrier out"), (16, "upper start"), (17, "L1 done"), (10, "upper done"),
           (14, "finalize")]

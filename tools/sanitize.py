@@ -48,7 +48,6 @@ case("loop_kernel_m15_lut", m=1.5)
 case("per_pass_graph", opts=((_lib.FCM_OPT_LOOP, 0),))
 case("per_pass_host", opts=((_lib.FCM_OPT_LOOP, 0), (_lib.FCM_OPT_GRAPH, 0)))
 case("prologue_kernel", opts=((_lib.FCM_OPT_SEED_PASS, 0),))
-case("ldg_kernel", opts=((_lib.FCM_OPT_KERNEL, 1),), table=False)
 case("recompute", opts=((_lib.FCM_OPT_RECOMPUTE, 1),))
 case("shards4", devices=[0, 0, 0, 0], opts=((_lib.FCM_OPT_PEER_TIMEOUT_MS, 2000),))
 case("u16", kind=_lib.FCM_X_U16, x=(x8.astype(np.uint16) * 200))
