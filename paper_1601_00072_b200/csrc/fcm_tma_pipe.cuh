@@ -384,21 +384,26 @@ __device__ __forceinline__ int tma_produce(const PassArgs& a, uint8_t* smem, Pip
   int claimed = 0;
   const int off = first_static ? (int)gridDim.x : 0;
   bool aborted = false;
+  // one tile per CTA (grid == tiles): nothing to claim -- the end-of-pass
+  // marker follows the static tile at once and the gate comes after it
+  const bool static_only = first_static && ntiles <= (int)gridDim.x;
+  auto pass_gate = [&]() {  // the previous pass's barrier, then the reducer's gate
+    if (gate->target && !wait_count(const_cast<unsigned*>(gate->bar_count), gate->target)) aborted = true;
+    fence_proxy_async_global();  // other CTAs' u_{k-1} (acquired above) before the bulk copies
+    mbar_arrive(gate->mbar);     // (release, CTA scope) -> the reducer may reset slots
+  };
   for (;;) {
-    if (gate && claimed == 1) {  // the static tile is out: now the previous pass's barrier
-      if (gate->target && !wait_count(const_cast<unsigned*>(gate->bar_count), gate->target)) aborted = true;
-      fence_proxy_async_global();  // other CTAs' u_{k-1} (acquired above) before the bulk copies
-      mbar_arrive(gate->mbar);     // (release, CTA scope) -> the reducer may reset slots
-    }
+    if (gate && claimed == 1 && !static_only) pass_gate();  // the static tile is out
     // (mod 2^32: a monotone counter)
     const int lt = (first_static && claimed == 0) ? (int)blockIdx.x
-                   : aborted                     ? ntiles
+                   : (aborted || static_only)    ? ntiles
                                                  : (int)(atomicAdd(counter, 1u) - base) + off;
     if (lt >= ntiles) {
       mbar_wait(bar0 + 8u * (S + ps.stage), ps.phase ^ 1u);
       meta[ps.stage].tile = -1;
       mbar_arrive(bar0 + 8u * ps.stage);
       ps.advance<S>();
+      if (gate && static_only) pass_gate();
       return aborted ? -1 : claimed;
     }
     ++claimed;

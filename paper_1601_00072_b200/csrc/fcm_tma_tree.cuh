@@ -146,16 +146,7 @@ __device__ __forceinline__ void tma_reduce(const PassArgs& a, RedSlots<2 * C + 2
                                 : (mbar_wait(smem_u32(&rs.full[sp.stage]), sp.phase), true))) {
       const int t = rs.tile[sp.stage];
       if (t >= 0) {
-        // (loop kernel, small volumes: the slot this tile takes two passes
-        // from now is reset to unpublished -- once the producer has seen the
-        // previous pass's grid barrier, i.e. every CTA has finished reading
-        // the pass that last used it)
-        if (tile_reset && !reset_ok) {
-          mbar_wait(gate_mbar, gate_parity);  // this pass's phase of the producer's gate
-          reset_ok = true;
-        }
         for (int f = lane; f < nf; f += 32) {  // nf <= 34
-          if (tile_reset) st_relaxed(tile_reset + (int64_t)t * nf + f, sentinel());
           const bool mx = f == nf - 1;
           const double(*w)[NF] = rs.w[sp.stage];
           const double q0 = combine(w[0][f], w[1][f], mx);
@@ -170,6 +161,18 @@ __device__ __forceinline__ void tma_reduce(const PassArgs& a, RedSlots<2 * C + 2
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(&rs.empty[sp.stage]));
       sp.advance<kSlots>();
+      // (loop kernel, small volumes: the slot tile t takes two passes from
+      // now is reset to unpublished -- after the partial is out, and once the
+      // producer has seen the previous pass's grid barrier, i.e. every CTA
+      // has finished reading the pass that last used it; before this CTA's
+      // own barrier arrival, which the resets must precede)
+      if (tile_reset && t >= 0) {
+        if (!reset_ok) {
+          mbar_wait(gate_mbar, gate_parity);  // this pass's phase of the producer's gate
+          reset_ok = true;
+        }
+        for (int f = lane; f < nf; f += 32) st_relaxed(tile_reset + (int64_t)t * nf + f, sentinel());
+      }
       if (LOOP && slots_done) {
         bar_arrive_end();  // the CTA may enter the grid barrier now
         if (it && lane == 0) probe(a, it, 15, global_ns());
