@@ -577,6 +577,18 @@ int build_graph(fcm_plan* p, double eps, int max_iters) {
 // host-side row expansion for fcm_download_table (below)
 namespace {
 
+// SM count of a device, cached (the seam ops size their grids by it).
+int device_sms(int device) {
+  static int cache[64] = {0};
+  if (device < 0 || device >= 64) return 148;
+  if (!cache[device]) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) != cudaSuccess || v < 1) v = 148;
+    cache[device] = v;
+  }
+  return cache[device];
+}
+
 template <int C>
 void expand_u_c(const uint8_t* x, int64_t i0, int64_t i1, const double* tab, double* u) {
   double* o = u + i0 * C;
@@ -1431,61 +1443,32 @@ int fcm_fill_membership_random(double* u_out, int64_t n, int32_t c, uint64_t see
 int fcm_update_centers(const double* x, const double* u, double* v_out, int64_t n, int32_t c,
                        double m, int32_t device, int32_t* dead_out) {
   if (!x || !u || !v_out || n < 1 || c < 1 || c > kCMaxSupported || !(m > 1.0)) return FCM_E_ARG;
-  // One plan, prologue only: the same fused sums the loop uses for v_1.
-  // c == 1 is legal here (the reference's tests use a 1-column membership),
-  // so the plan is built for c >= 2 with zero padding columns ignored.
-  fcm_plan* p = nullptr;
-  const int cp = c < 2 ? 2 : c;
-  int rc = fcm_plan_create(&p, std::max<int64_t>(n, cp), cp, FCM_X_F64, 1, &device);
-  if (rc) return rc;
-  std::vector<double> xx(x, x + n), uu;
-  const double* up = u;
-  if (c != cp || n < cp) {
-    const int64_t nn = std::max<int64_t>(n, cp);
-    xx.assign(nn, 0.0);
-    std::copy(x, x + n, xx.begin());
-    uu.assign(nn * cp, 0.0);
-    for (int64_t i = 0; i < n; ++i)
-      for (int j = 0; j < c; ++j) uu[i * cp + j] = u[i * c + j];
-    for (int j = c; j < cp; ++j) uu[j] = 1.0;  // keep padding columns alive
-    up = uu.data();
-    if (n < nn) {
-      // padding voxels must not contribute: give them zero membership
-      for (int64_t i = n; i < nn; ++i)
-        for (int j = 0; j < cp; ++j) uu[i * cp + j] = 0.0;
+  // One seam op, no plan: the 2c sums of Eq. 3 over the caller's AoS rows
+  // (op_center_sums: per-CTA voxel ranges, fixed trees), then the
+  // reference's control flow -- the first cluster with zero total weight is
+  // dead and ends the update (_kernels.pyx:79-89).
+  CKS(cudaSetDevice(device));
+  DevBuf dx, du, ds, dw;
+  CKS(cudaMalloc(&dx.p, sizeof(double) * n));
+  CKS(cudaMalloc(&du.p, sizeof(double) * n * c));
+  CKS(cudaMalloc(&ds.p, sizeof(double) * kCenterScratch));
+  CKS(cudaMalloc(&dw.p, sizeof(double) * 2 * c));
+  CKS(cudaMemcpy(dx.p, x, sizeof(double) * n, cudaMemcpyHostToDevice));
+  CKS(cudaMemcpy(du.p, u, sizeof(double) * n * c, cudaMemcpyHostToDevice));
+  CKS(op_center_sums((const double*)dx.p, (const double*)du.p, n, c, m, (double*)ds.p, (double*)dw.p,
+                     device_sms(device), 0));
+  std::vector<double> sums(2 * c);
+  CKS(cudaMemcpy(sums.data(), dw.p, sizeof(double) * 2 * c, cudaMemcpyDeviceToHost));
+  int dead = -1;
+  for (int j = 0; j < c; ++j) {
+    if (sums[c + j] == 0.0) {
+      dead = j;
+      break;
     }
+    v_out[j] = sums[j] / sums[c + j];
   }
-  rc = fcm_upload_pixels(p, xx.data());
-  if (!rc) rc = fcm_upload_membership(p, up);
-  if (!rc) {
-    set_powers(p, m);
-    Control tmpl;
-    memset(&tmpl, 0, sizeof tmpl);
-    tmpl.dead = -1;
-    Shard& s = p->sh[0];
-    cudaSetDevice(s.device);
-    if (s.trace_cap < 1) rc = dalloc(p, s, &s.trace, 2), s.trace_cap = 1;
-    if (!rc) {
-      *p->host_tmpl = tmpl;
-      cudaMemcpyAsync(s.ctl, p->host_tmpl, sizeof tmpl, cudaMemcpyHostToDevice, s.stream);
-      cudaMemsetAsync(s.node_cnt[1], 0, sizeof(unsigned) * s.cnt_total, s.stream);
-      rc = step(p, 0, 0.5, 1);
-      if (!rc && cudaStreamSynchronize(s.stream) != cudaSuccess) rc = FCM_E_CUDA;
-    }
-    if (!rc) {
-      Control h;
-      if (cudaMemcpy(&h, s.ctl, sizeof h, cudaMemcpyDeviceToHost) != cudaSuccess) rc = FCM_E_CUDA;
-      else {
-        int dead = -1;
-        for (int j = 0; j < c; ++j)
-          if (h.root[cp + j] == 0.0) { dead = j; break; }
-        if (dead_out) *dead_out = dead;
-        for (int j = 0; j < c && (dead < 0 || j < dead); ++j) v_out[j] = h.root[j] / h.root[cp + j];
-      }
-    }
-  }
-  fcm_plan_destroy(p);
-  return rc;
+  if (dead_out) *dead_out = dead;
+  return FCM_OK;
 }
 
 int fcm_update_membership(const double* x, const double* v, double* u_out, int64_t n, int32_t c,
@@ -1519,7 +1502,7 @@ int fcm_update_membership(const double* x, const double* v, double* u_out, int64
     memcpy(u_out, ones.data(), sizeof(double) * n);
     return FCM_OK;
   }
-  CKS(launch_epilogue(XK_F64, c, tmp.mode, e, 148, 0));
+  CKS(launch_epilogue(XK_F64, c, tmp.mode, e, device_sms(device), 0));
   CKS(cudaMemcpy(u_out, du.p, sizeof(double) * n * c, cudaMemcpyDeviceToHost));
   return FCM_OK;
 }

@@ -239,12 +239,22 @@ __device__ __forceinline__ void tile_finish(const PassArgs& a, int lt, const dou
   constexpr int NS = 2 * C + 2;
   const int c = C <= 8 ? C : a.c, nf = 2 * c + 2;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // lanes -> warp value: the sum fields through the halving butterfly (the
+  // same tile-internal tree as the TMA consumers), the max field through a
+  // warp tree (max is order-free)
+  constexpr int NSUM = NS - 1;
+  double v[NSUM];
 #pragma unroll
-  for (int s = 0; s < NS; ++s) {
-    double r = warp_tree(acc[s], s == NS - 1);
-    int f = field_of<C>(s, c);
-    if (lane == 0 && f >= 0) sm.w[buf][warp][f] = r;
+  for (int s = 0; s < NSUM; ++s) v[s] = acc[s];
+  bfly_level<NSUM, 16>(v, lane);
+#pragma unroll
+  for (int k = 0; k < bfly_slots(NSUM); ++k) {
+    const int s = bfly_field(lane, NSUM, k);
+    const int f = s >= 0 ? field_of<C>(s, c) : -1;
+    if (f >= 0) sm.w[buf][warp][f] = v[k];
   }
+  const double dm = warp_tree(acc[NS - 1], true);
+  if (lane == 0) sm.w[buf][warp][field_of<C>(NS - 1, c)] = dm;
   red_sync<NAMED>();
   if (warp != 0) return;
   for (int f = lane; f < nf; f += 32) {  // nf <= 34
@@ -518,7 +528,7 @@ __global__ void __launch_bounds__(kThreads) epilogue_kernel(EpilogueArgs a) {
 }
 
 }  // namespace fcm
-#include "fcm_pass_tma.cuh"
+#include "fcm_tma_kernels.cuh"
 namespace fcm {
 
 // ------------------------------------------------------------ launchers ---

@@ -60,6 +60,65 @@ __global__ void terms_kernel(int kind, const double* x, const double* u, const d
   if (threadIdx.x == 0) partials[blockIdx.x] = r;
 }
 
+// Eq. 3 sums of the seam (update_centers_linear, _kernels.pyx:72-90) on the
+// reference's AoS fp64 membership: fields [f0, f0 + 16) of the 2c sums
+// (f < c: sum pow(u_if, m) x_i; f >= c: sum pow(u_i(f-c), m)), each CTA over
+// one contiguous voxel range, block tree per field -> partials[block][16].
+constexpr int kCenterFields = 16;
+__global__ void centers_terms_kernel(const double* x, const double* u, int64_t n, int c, double m, int f0,
+                                     double* partials) {
+  const int64_t chunk = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t lo = (int64_t)blockIdx.x * chunk;
+  const int64_t hi = lo + chunk < n ? lo + chunk : n;
+  const int nfk = min(kCenterFields, 2 * c - f0);
+  double acc[kCenterFields];
+#pragma unroll
+  for (int k = 0; k < kCenterFields; ++k) acc[k] = 0.0;
+  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+    const double xi = x[i];
+#pragma unroll
+    for (int k = 0; k < kCenterFields; ++k) {
+      const int f = f0 + k;
+      if (k < nfk) {
+        const double w = pow(u[i * c + (f < c ? f : f - c)], m);
+        acc[k] += f < c ? w * xi : w;
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < kCenterFields; ++k) {
+    const double r = block_tree(acc[k], false);
+    if (threadIdx.x == 0) partials[blockIdx.x * kCenterFields + k] = r;
+  }
+}
+
+// One CTA per field: fold the per-CTA partials of field k (stride 16) in a fixed order.
+__global__ void centers_fold_kernel(const double* partials, int np, int f0, int nfk, double* out) {
+  const int k = blockIdx.x;
+  if (k >= nfk) return;
+  double acc = 0.0;
+  const int per = (np + blockDim.x - 1) / blockDim.x;
+  for (int q = 0; q < per; ++q) {
+    const int i = threadIdx.x * per + q;
+    if (i < np) acc += partials[i * kCenterFields + k];
+  }
+  const double r = block_tree(acc, false);
+  if (threadIdx.x == 0) out[f0 + k] = r;
+}
+
+cudaError_t op_center_sums(const double* x, const double* u, int64_t n, int c, double m, double* scratch,
+                           double* sums, int sms, cudaStream_t st) {
+  int blocks = (int)std::min<int64_t>((n + 4095) / 4096, (int64_t)sms * 4);
+  if (blocks > kOpsBlocks) blocks = kOpsBlocks;
+  if (blocks < 1) blocks = 1;
+  for (int f0 = 0; f0 < 2 * c; f0 += kCenterFields) {
+    centers_terms_kernel<<<blocks, kThreads, 0, st>>>(x, u, n, c, m, f0, scratch);
+    centers_fold_kernel<<<kCenterFields, kThreads, 0, st>>>(scratch, blocks, f0, std::min(kCenterFields, 2 * c - f0),
+                                                            sums);
+  }
+  return cudaGetLastError();
+}
+
 __global__ void partials_kernel(const double* partials, int np, bool is_max, double* out) {
   // np <= blockDim.x * k: each thread folds a contiguous run, then the block tree.
   double acc = 0.0;

@@ -10,6 +10,11 @@ cudaError_t op_init_aos(double* u, int64_t n, int c, uint64_t seed, cudaStream_t
 cudaError_t op_reduce(int kind, const double* x, const double* u, const double* v, int64_t n, int c,
                       double m, const double* a, const double* b, double* scratch, double* out,
                       cudaStream_t st);
+// Eq. 3 sums of update_centers_linear on AoS fp64 u: sums[0..c) = sum pow(u_ij, m) x_i,
+// sums[c..2c) = sum pow(u_ij, m); scratch holds kOpsBlocks * 16 doubles.
+constexpr int kCenterScratch = 1024 * 16;
+cudaError_t op_center_sums(const double* x, const double* u, int64_t n, int c, double m, double* scratch,
+                           double* sums, int sms, cudaStream_t st);
 cudaError_t op_argmax(const double* u, int32_t* labels, int64_t n, int c, cudaStream_t st);
 // Label statistics of a solve (metrics): bins[p*cref + r] += |pred==p & ref==r| when ref is set;
 // bins[p] += |pred==p & mask|, bins[c] += |mask|, bins[c+1+p] += |pred==p| when mask is set.

@@ -1,7 +1,7 @@
 // fcm_tma_pipe.cuh -- the streaming half of the TMA pass: PTX glue, stage
 // ring layout, producer (bulk copies), intensity tables and the consumer
 // warps (per-voxel Eq. 4 / Eq. 3 terms, tile-end hand-off to the reducer).
-// Part of fcm_pass_tma.cuh.
+// Part of the TMA pass (fcm_tma_kernels.cuh).
 #pragma once
 #include <climits>
 
@@ -591,16 +591,22 @@ __device__ __forceinline__ void tma_consume_seed(const PassArgs& a, uint8_t* sme
     for (int j = 0; j < C; ++j)
       if (j < c) st_u4(reinterpret_cast<float4*>(a.u_nxt + j * a.g.plane + i0), un[j], keep, pol);
     if (mt.last) {
-      double r[NS];
+      // the sum fields through the halving butterfly (bfly_level); the
+      // pass-0 delta and objective fields are 0.0
+      constexpr int NSUM = NS - 1;
+      double v[NSUM];
 #pragma unroll
-      for (int s2 = 0; s2 < NS; ++s2) r[s2] = warp_tree(acc[s2], s2 == NS - 1);
+      for (int s2 = 0; s2 < NSUM; ++s2) v[s2] = acc[s2];
+      bfly_level<NSUM, 16>(v, tid & 31);
       mbar_wait(smem_u32(&rs.empty[sp.stage]), sp.phase ^ 1u);
-      if ((tid & 31) == 0) {
 #pragma unroll
-        for (int s2 = 0; s2 < NS; ++s2) {
-          const int f = field_of<C>(s2, c);
-          if (f >= 0) rs.w[sp.stage][tid >> 5][f] = r[s2];
-        }
+      for (int k = 0; k < bfly_slots(NSUM); ++k) {
+        const int s2 = bfly_field(tid & 31, NSUM, k);
+        const int f = s2 >= 0 ? field_of<C>(s2, c) : -1;
+        if (f >= 0) rs.w[sp.stage][tid >> 5][f] = v[k];
+      }
+      if ((tid & 31) == 0) {
+        rs.w[sp.stage][tid >> 5][field_of<C>(NS - 1, c)] = 0.0;
         if (tid == 0) rs.tile[sp.stage] = mt.tile;
       }
       __syncwarp();
@@ -762,20 +768,28 @@ __device__ __forceinline__ void tma_consume(const PassArgs& a, uint8_t* smem, Pi
         acc[2 * C] = cd * ljb;
         hpar ^= 1;
       }
-      acc[2 * C + 1] = LUT ? (double)dmax_f : __hiloint2double((int)dmax_hi, (int)0xffffffffu);
-      // lanes -> warp value per field (adjacent-pair tree), then hand the
-      // 8 warp values to the reducer through a slot
+      // lanes -> warp value per field: the sum fields through the halving
+      // butterfly (bfly_level: the tile-internal tree), the delta as one
+      // max reduction of its order-preserving 32-bit key (the fp32 delta, or
+      // the high word of the fp64 one) -- then hand the 8 warp values to the
+      // reducer through a slot
       constexpr int NS = 2 * C + 2;
-      double r[NS];
+      constexpr int NSUM = NS - 1;
+      double v[NSUM];
 #pragma unroll
-      for (int s2 = 0; s2 < NS; ++s2) r[s2] = warp_tree(acc[s2], s2 == NS - 1);
+      for (int s2 = 0; s2 < NSUM; ++s2) v[s2] = acc[s2];
+      bfly_level<NSUM, 16>(v, tid & 31);
+      const uint32_t dkey = __reduce_max_sync(0xffffffffu, LUT ? __float_as_uint(dmax_f) : dmax_hi);
       mbar_wait(smem_u32(&rs.empty[sp.stage]), sp.phase ^ 1u);
-      if ((tid & 31) == 0) {
 #pragma unroll
-        for (int s2 = 0; s2 < NS; ++s2) {
-          const int f = field_of<C>(s2, c);
-          if (f >= 0) rs.w[sp.stage][tid >> 5][f] = r[s2];
-        }
+      for (int k = 0; k < bfly_slots(NSUM); ++k) {
+        const int s2 = bfly_field(tid & 31, NSUM, k);
+        const int f = s2 >= 0 ? field_of<C>(s2, c) : -1;
+        if (f >= 0) rs.w[sp.stage][tid >> 5][f] = v[k];
+      }
+      if ((tid & 31) == 0) {
+        rs.w[sp.stage][tid >> 5][field_of<C>(NS - 1, c)] =
+            LUT ? (double)__uint_as_float(dkey) : __hiloint2double((int)dkey, (int)0xffffffffu);
         if (tid == 0) rs.tile[sp.stage] = mt.tile;
       }
       __syncwarp();

@@ -1,7 +1,7 @@
 // fcm_tma_tree.cuh -- the reduction half of the TMA pass: reducer warp,
 // fence-free publication of tile partials, level-1 owners, the upper tree
 // levels, the grid barrier, the loop kernel's stop test and the multi-rank
-// mailbox exchange.  Part of fcm_pass_tma.cuh.
+// mailbox exchange.  Part of the TMA pass (fcm_tma_kernels.cuh).
 #pragma once
 #include "fcm_tma_pipe.cuh"
 

@@ -124,3 +124,18 @@ def test_seeded_pass_equals_uploaded_reference_rows():
             v2, trace2, k2, conv2 = plan.run(2.0, 1e-300, 3)
         assert k == k2 == 3
         assert v.tobytes() == v2.tobytes() and trace.tobytes() == trace2.tobytes()
+
+
+@pytest.mark.parametrize("n,c,m", [(1_000_003, 5, 2.0), (300_001, 20, 1.5), (70_000, 1, 2.0)])
+def test_update_centers_seam_large(n, c, m):
+    """The seam's Eq. 3 (one op, no plan; 2c sums per CTA range and fixed
+    trees, update_centers_linear, _kernels.pyx:72-90) against the oracle's
+    restatement of the reference on the same AoS rows, up to c = 20."""
+    from oracle import oracle as O
+    rng = np.random.default_rng(n)
+    x = rng.integers(0, 256, n).astype(np.float64)
+    u = O.fill_membership_random(n, c, 99) if c > 1 else np.ones(n)
+    v, dead = O.update_centers_linear(x, u.reshape(-1), c, m)
+    got = pkg.update_centers(pkg.GrayImage(n, 1, x), pkg.MembershipMatrix(n, c, u.reshape(-1)), m).v
+    assert dead < 0
+    assert np.allclose(got, v, rtol=1e-11, atol=0)

@@ -12,3 +12,4 @@ for f in C2_1 C4_1 C2_2 C4_2; do python -c "
 import json,sys; d=json.load(open('gpurun_out/bench_$f.json')); print('$f', d['value']/1e9, 'G', d['ms_per_step'], 'ms', d['roofline']['frac'], d.get('clocks'))" ; done
 grep -E "^C|solve|next" gpurun_out/pass_phases.txt
 if [ -n "$SAN" ]; then bash tools/gpu_sanitize.sh; fi
+if [ -n "$E2E" ]; then timeout 900 python tools/e2e_phases.py > gpurun_out/e2e_phases.txt 2>&1; cat gpurun_out/e2e_phases.txt; fi
