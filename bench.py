@@ -291,7 +291,9 @@ def run_ours(args, rank, world, local_rank, dist):
     plan.init_membership(0)
     plan.set_option(_lib.FCM_OPT_KERNEL, KERNELS[args.kernel])
     plan.set_option(_lib.FCM_OPT_LOOP, 0 if args.no_loop else 1)
-    plan.set_option(_lib.FCM_OPT_SEED_PASS, 0 if args.no_seed_pass else 1)
+    # seeded start: auto (pass 0 of the loop kernel for small volumes, the
+    # prologue kernel for large ones) unless forced
+    plan.set_option(_lib.FCM_OPT_SEED_PASS, 0 if args.no_seed_pass else (1 if args.seed_in_loop else 2))
 
     def barrier():
         if world > 1:
@@ -619,7 +621,9 @@ def main():
     ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
                     help="N>1 root exchange: in-kernel peer-memory mailboxes (p2p) or ncclAllGather per pass")
     ap.add_argument("--no-seed-pass", action="store_true",
-                    help="separate prologue kernel for the seeded start instead of the loop kernel's pass 0")
+                    help="seeded start always in the separate prologue kernel")
+    ap.add_argument("--seed-in-loop", action="store_true",
+                    help="seeded start always as the loop kernel's pass 0 (default: auto by volume)")
     ap.add_argument("--no-loop", action="store_true",
                     help="one launch per pass (CUDA graph with a conditional node) instead of the persistent loop kernel")
     ap.add_argument("--kernel", default="tma", choices=sorted(KERNELS),

@@ -68,8 +68,9 @@ typedef enum {
   FCM_OPT_L2 = 7,      /* 0: stream x/u with evict-first stores; 1 (default): keep them in L2
                           (evict_last policy) when they fit; 2: always */
   FCM_OPT_PROFILE = 8, /* 1: the loop kernel records a per-CTA timeline (fcm_last_profile) */
-  FCM_OPT_SEED_PASS = 9, /* 1 (default): with a seeded start the loop kernel generates u_0 as its
-                           pass 0; 0: a separate prologue kernel does */
+  FCM_OPT_SEED_PASS = 9, /* seeded start: 1 = the loop kernel generates u_0 as its pass 0, 0 = a
+                           separate prologue kernel does, 2 (default) = auto: pass 0 for volumes of
+                           <= 1024 tiles and in recompute mode, the prologue kernel above */
   FCM_OPT_RECOMPUTE = 11, /* 1: "effective" mode (uint8 pixels, m == 2, seeded start, loop kernel):
                            passes >= 2 read x only and write u_k; delta_k is taken between the fp64
                            intensity tables of passes k-1 and k over the intensities present

@@ -145,7 +145,7 @@ struct fcm_plan {
   int use_loop = 1;
   int l2_mode = 1;  // 0 never keep x/u in L2, 1 when they fit (default), 2 always
   int profile = 0;  // record the loop kernel's per-CTA timeline
-  int seed_pass = 1;  // loop kernel generates the seeded u_0 as its pass 0
+  int seed_pass = 2;  // seeded u_0: 1 = loop kernel's pass 0, 0 = prologue kernel, 2 = auto (by volume)
   int recompute = 0;  // loop kernel: "effective" mode, passes >= 2 stream x only
   std::vector<double> deltas;  // delta_1..delta_k of the last fcm_run
   std::vector<double> res_tab_u;  // the 256-row result table of the last fcm_download_table
@@ -573,6 +573,8 @@ int build_graph(fcm_plan* p, double eps, int max_iters) {
 }
 }  // namespace
 
+constexpr int kSmallTilesHost = 1024;  // = kSmallTiles (fcm_tma_pipe.cuh): the loop kernel's small-volume bound
+
 // ================================================================== C ABI ==
 // host-side row expansion for fcm_download_table (below)
 namespace {
@@ -800,7 +802,10 @@ int fcm_set_option(fcm_plan* p, int32_t key, int64_t value) {
     case FCM_OPT_GRAPH: p->use_graph = value ? 1 : 0; return FCM_OK;
     case FCM_OPT_LOOP: p->use_loop = value ? 1 : 0; return FCM_OK;
     case FCM_OPT_PROFILE: p->profile = value ? 1 : 0; return FCM_OK;
-    case FCM_OPT_SEED_PASS: p->seed_pass = value ? 1 : 0; return FCM_OK;
+    case FCM_OPT_SEED_PASS:
+      if (value < 0 || value > 2) return FCM_E_ARG;
+      p->seed_pass = (int)value;
+      return FCM_OK;
     case FCM_OPT_RECOMPUTE: p->recompute = value ? 1 : 0; return FCM_OK;
     case FCM_OPT_DEBUG_DELAY:
       if (value < 0 || value > 10000000) return FCM_E_ARG;  // <= 10 ms
@@ -946,7 +951,14 @@ static int run_impl(fcm_plan* p, double m, double eps, int32_t max_iters, double
     CK(cudaEventRecord(p->ev_start, s0.stream));
     // seeded start: pass 0 of the loop kernel (no prologue launch);
     // uploaded start: the prologue kernel reads the AoS rows first
-    const bool seed_pass = p->init_src == 1 && p->seed_pass;
+    // auto: small volumes generate u_0 inside the loop kernel (no second
+    // launch); large ones in the prologue kernel, which runs the
+    // SplitMix64-bound work at 4 CTAs per SM instead of the loop kernel's 2
+    // (C4: 0.75 vs 0.84 ms; same v_1 bit for bit); recompute mode needs the
+    // in-loop pass 0 (it records the intensities present)
+    const bool small = p->sh[0].g.tiles_local <= kSmallTilesHost;
+    const bool seed_pass = p->init_src == 1 &&
+                           (p->seed_pass == 1 || (p->seed_pass == 2 && (small || p->recompute)));
     if (!seed_pass && (rc = step(p, 0, eps, max_iters))) return rc;
     for (int i = 1; i < p->nshards; ++i) {  // shards start together with shard 0
       CK(cudaSetDevice(p->sh[i].device));

@@ -455,13 +455,20 @@ __global__ void __launch_bounds__(kThreads, C <= 4 ? 4 : 2) prologue_kernel(Pass
     for (int s = 0; s < 2 * C + 2; ++s) acc[s] = 0.0;
     const int64_t base = (int64_t)lt << a.g.tile_shift;
     // 4 consecutive voxels per thread per 1024-voxel chunk, chunk by chunk:
-    // the TMA pass's map, so both give the same tile partials bit for bit
+    // the TMA pass's map, so both give the same tile partials bit for bit.
+    // The next chunk's pixels are loaded before this chunk's rows are
+    // generated (x is padded to whole tiles), so the load latency hides
+    // behind the SplitMix64 work instead of stalling it.
+    double xn[4];
+    XLoad<XT>::load4(reinterpret_cast<const XT*>(a.x), base + threadIdx.x * kVec, xn);
     for (int ch = 0; ch < chunks; ++ch) {
       const int64_t i0 = base + (int64_t)ch * (kThreads * kVec) + threadIdx.x * kVec;
       const int64_t nvalid = a.g.n_local - i0;
       if (nvalid <= 0) break;
       double xd[4];
-      XLoad<XT>::load4(reinterpret_cast<const XT*>(a.x), i0, xd);  // x is padded to whole tiles
+#pragma unroll
+      for (int q = 0; q < 4; ++q) xd[q] = xn[q];
+      if (ch + 1 < chunks) XLoad<XT>::load4(reinterpret_cast<const XT*>(a.x), i0 + kThreads * kVec, xn);
       float4 un[C];
       if (FROM_SEED) {
         seed_quad<C, MODE>(a, pw, c, i0, xd, nvalid, un, acc);
