@@ -36,7 +36,7 @@ __device__ __forceinline__ void tma_init_barriers(uint8_t* smem, RedSlots<2 * C 
     mbar_init(bar0 + 8u * (L::kStages + s), kWarps);
   }
   for (int s = 0; s < kSlots; ++s) {
-    mbar_init(smem_u32(&rs.full[s]), kWarps);
+    mbar_init(smem_u32(&rs.full[s]), kThreads);
     mbar_init(smem_u32(&rs.empty[s]), 1);
   }
   mbar_fence_init();

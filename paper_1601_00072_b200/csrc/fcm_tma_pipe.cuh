@@ -17,8 +17,9 @@ constexpr int kSlots = 8;  // tile-partial slots between consumers and the reduc
 constexpr int kSmallTiles = 1024;  // loop kernel: up to this many tiles every CTA reduces level 1 itself
 
 // Consumer -> reducer handoff: per slot, the 8 warp-tree values of every
-// field of one tile (tile = -1: end of pass).  full: 8 warp arrivals;
-// empty: 1 reducer arrival.
+// field of one tile (tile = -1: end of pass).  full: one arrival per
+// consumer thread (after the butterfly several lanes of a warp write fields,
+// and each releases its own writes); empty: 1 reducer arrival.
 template <int NF>
 struct RedSlots {
   double w[kSlots][kWarps][NF];
@@ -547,8 +548,7 @@ __device__ __forceinline__ void tma_consume_seed(const PassArgs& a, uint8_t* sme
       }
       mbar_wait(smem_u32(&rs.empty[sp.stage]), sp.phase ^ 1u);
       if (tid == 0) rs.tile[sp.stage] = -1;
-      __syncwarp();
-      if ((tid & 31) == 0) mbar_arrive(smem_u32(&rs.full[sp.stage]));
+      mbar_arrive(smem_u32(&rs.full[sp.stage]));  // every consumer thread: its own slot writes
       sp.advance<kSlots>();
       return;
     }
@@ -609,8 +609,7 @@ __device__ __forceinline__ void tma_consume_seed(const PassArgs& a, uint8_t* sme
         rs.w[sp.stage][tid >> 5][field_of<C>(NS - 1, c)] = 0.0;
         if (tid == 0) rs.tile[sp.stage] = mt.tile;
       }
-      __syncwarp();
-      if ((tid & 31) == 0) mbar_arrive(smem_u32(&rs.full[sp.stage]));
+      mbar_arrive(smem_u32(&rs.full[sp.stage]));  // every consumer thread: its own slot writes
       sp.advance<kSlots>();
 #pragma unroll
       for (int s = 0; s < NS; ++s) acc[s] = 0.0;
@@ -659,8 +658,7 @@ __device__ __forceinline__ void tma_consume(const PassArgs& a, uint8_t* smem, Pi
       // end-of-pass slot for the reducer
       mbar_wait(smem_u32(&rs.empty[sp.stage]), sp.phase ^ 1u);
       if (tid == 0) rs.tile[sp.stage] = -1;
-      __syncwarp();
-      if ((tid & 31) == 0) mbar_arrive(smem_u32(&rs.full[sp.stage]));
+      mbar_arrive(smem_u32(&rs.full[sp.stage]));  // every consumer thread: its own slot writes
       sp.advance<kSlots>();
       return;
     }
@@ -792,8 +790,7 @@ __device__ __forceinline__ void tma_consume(const PassArgs& a, uint8_t* smem, Pi
             LUT ? (double)__uint_as_float(dkey) : __hiloint2double((int)dkey, (int)0xffffffffu);
         if (tid == 0) rs.tile[sp.stage] = mt.tile;
       }
-      __syncwarp();
-      if ((tid & 31) == 0) mbar_arrive(smem_u32(&rs.full[sp.stage]));
+      mbar_arrive(smem_u32(&rs.full[sp.stage]));  // every consumer thread: its own slot writes
       sp.advance<kSlots>();
 #pragma unroll
       for (int s = 0; s < 2 * C + 2; ++s) acc[s] = 0.0;

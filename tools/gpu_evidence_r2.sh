@@ -5,7 +5,7 @@ cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out/parity
 FCM_PARITY_LOG=gpurun_out/parity timeout 1500 python -m pytest tests -m gpu -q --timeout 600 -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
-bash tools/gpu_sanitize.sh > gpurun_out/sanitize_summary.txt 2>&1
+if [ -n "$SAN" ]; then bash tools/gpu_sanitize.sh > gpurun_out/sanitize_summary.txt 2>&1; fi
 timeout 900 python bench.py > gpurun_out/bench_C4.json 2> gpurun_out/bench_C4.err
 timeout 900 python bench.py --impl reference --steps 5 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
 timeout 600 python bench.py --config C2 --no-cpu-baseline > gpurun_out/bench_C2.json 2> gpurun_out/bench_C2.err
