@@ -145,13 +145,20 @@ __global__ void __launch_bounds__(kTmaThreads, 2) loop_tma_kernel(PassArgs a) {
   // the producer of the next pass, after its static first tile (whose
   // u_{k-1} this CTA wrote itself), before it claims tiles other CTAs wrote.
   const bool proto_s = fusedP != 0 && !a.debug_shared_parts;
+  // the same for large volumes (level-1 owners): owners read this pass's
+  // tile-partial buffer without resetting it, publish each level-1 result
+  // with relaxed stores into l1_buf[g % 3] and reset the node's slot of
+  // l1_buf[(g+1) % 3] (after the gate); after its stream every CTA arrives
+  // at the grid barrier and polls the level-1 results for the levels above
+  const bool proto_l = !from_tiles && !a.debug_shared_parts;
+  const bool proto = proto_s || proto_l;
   const int64_t tlen = (int64_t)a.g.tiles_local * (2 * a.c + 2);
   // recompute mode (SURVEY 8(d) "effective"): passes >= 2 stream x only;
   // u_{k-1} is never read back -- delta_k = max over the intensities present
   // of |u_k(b) - u_{k-1}(b)| from the two pass tables (fp64, exact)
   const bool recomp = a.recompute && MODE == MODE_LUT2 && sizeof(XT) == 1;
   unsigned l1_real = 0;  // real level-1 nodes of this rank (published once per pass)
-  if (!from_tiles)
+  if (!from_tiles && !proto_l)
     for (int lo = 0; lo < a.g.noct; ++lo) l1_real += (unsigned)octant_real_nodes(a.g, a.g.oct0 + lo, 1);
   Pipe ps, sp;
   // monotone tile scheduler: CTA b starts every pass with tile b (no claim),
@@ -179,7 +186,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) loop_tma_kernel(PassArgs a) {
     // (formed where used: a pointer live across the stream would cost the
     // consumers a register at the cap)
     auto tpart_of = [&](unsigned g) {
-      return a.tile_part + (proto_s ? (int64_t)(g % 3u) * tlen
+      return a.tile_part + (proto ? (int64_t)(g % 3u) * tlen
                             : from_tiles && !a.debug_shared_parts ? (int64_t)(g & 1u) * tlen : 0);
     };
     if (tid >= kThreads) {
@@ -187,7 +194,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) loop_tma_kernel(PassArgs a) {
         fence_proxy_async_global();
         const ProduceGate gate{&a.ctl->bar_count, (gnext - 1u) * gridDim.x, smem_u32(&gatebar)};
         const int n = tma_produce<XT, C, MODE>(a, smem, ps, &a.ctl->tile_next[1], it, it == 0 || (recomp && it >= 2),
-                                                     sched, true, proto_s ? &gate : nullptr);
+                                                     sched, true, proto ? &gate : nullptr);
         if (n < 0) {
           a.ctl->dead = -3;  // a stuck CTA (cannot happen with co-resident CTAs): flag the run
           a.ctl->done = 1;
@@ -203,7 +210,8 @@ __global__ void __launch_bounds__(kTmaThreads, 2) loop_tma_kernel(PassArgs a) {
         // slots first (then arrive at the pass-end barrier), owned level-1
         // nodes after -- overlapping the grid barrier
         tma_reduce<C, true>(a, rs, sp, &a.ctl->tile_next[1], l1, it, from_tiles, sched, tpart_of(gnext),
-                            proto_s ? tpart_of(gnext + 1u) : nullptr, smem_u32(&gatebar), (gnext - 1u) & 1u);
+                            proto ? tpart_of(gnext + 1u) : nullptr, smem_u32(&gatebar), (gnext - 1u) & 1u,
+                            proto_l ? a.l1_buf + ((gnext + 1u) % 3u) * l1_len : nullptr);
         if ((tid & 31) == 0) probe(a, it, 7, global_ns());
       } else {
         bar_sync_end();
@@ -258,6 +266,28 @@ __global__ void __launch_bounds__(kTmaThreads, 2) loop_tma_kernel(PassArgs a) {
       const double xdelta = (recomp && it >= 2) ? sdelta : 0.0;
       const bool ok = loop_root_small<NF>(a, reinterpret_cast<double*>(smem), L::kRingBytes / 8, tpart, fusedP,
                                           rs.root, it, xdelta, 0u, &upphase, true);
+      if (!ok || s_abort) {
+        if (tid == 0) {
+          a.ctl->dead = -3;
+          a.ctl->done = 1;
+        }
+        break;
+      }
+    } else if (proto_l) {
+      if (tid == 0) {  // arrive (release: u_k and the owned level-1 results come later,
+        red_release_add(&a.ctl->bar_count, 1u);  // published by their own pattern), do not wait
+        probe(a, it, 3, global_ns());
+      }
+      if (a.debug_delay_ns) {  // race test: one CTA (a different one each pass) reads late
+        if (tid == 0 && blockIdx.x == (it * 7u + 1u) % gridDim.x) {
+          const uint64_t t0 = global_ns();
+          while (global_ns() - t0 < a.debug_delay_ns) __nanosleep(1000);
+        }
+        __syncthreads();
+      }
+      const double xdelta = (recomp && it >= 2) ? sdelta : 0.0;
+      const bool ok = loop_upper<NF>(a, l1, reinterpret_cast<double*>(smem), oroot, rs.root, it, false, xdelta,
+                                     0u, &upphase, L::kRingBytes / 8, nullptr, true);
       if (!ok || s_abort) {
         if (tid == 0) {
           a.ctl->dead = -3;

@@ -13,7 +13,7 @@ namespace fcm {
 // side effects, while any child is unpublished; otherwise resets the children
 // to unpublished and leaves the per-field adjacent-pair warp tree in lane 0
 // of out[f] (out in shared or global memory, written by lane 0).
-template <int NF, bool GLOBAL_OUT>
+template <int NF, bool GLOBAL_OUT, bool RESET = true>
 __device__ __forceinline__ bool try_node(double* child0, int nreal, int nf, double* out) {
   const int lane = threadIdx.x & 31;
   const bool real = lane < nreal;
@@ -30,7 +30,7 @@ __device__ __forceinline__ bool try_node(double* child0, int nreal, int nf, doub
 #pragma unroll
   for (int f = 0; f < NF; ++f)
     if (f < nf) {
-      if (real) st_relaxed(src + f, sentinel());
+      if (RESET && real) st_relaxed(src + f, sentinel());
       const double r = warp_tree(v[f], f == nf - 1);
       if (lane == 0) {
         if (GLOBAL_OUT) st_relaxed(out + f, r);
@@ -108,7 +108,8 @@ __device__ __forceinline__ void tma_reduce(const PassArgs& a, RedSlots<2 * C + 2
                                            const unsigned* counter, double* l1_out, unsigned it = 0,
                                            bool no_owners = false, unsigned base = 0,
                                            double* tile_out = nullptr, double* tile_reset = nullptr,
-                                           uint32_t gate_mbar = 0u, uint32_t gate_parity = 0u) {
+                                           uint32_t gate_mbar = 0u, uint32_t gate_parity = 0u,
+                                           double* l1_reset = nullptr) {
   constexpr int NF = 2 * C + 2;
   const int lane = threadIdx.x & 31;
   const int nf = 2 * a.c + 2;
@@ -202,12 +203,26 @@ __device__ __forceinline__ void tma_reduce(const PassArgs& a, RedSlots<2 * C + 2
       // (loop kernel: tiles 0..G-1 are every CTA's static first tile, the
       // counter hands out G..)
       node_hot = (LOOP && slots_done) || (int)(ld_relaxed_u32(counter) - base) + (LOOP ? G : 0) > last_lt;
+      if (node_hot && l1_reset && !reset_ok) {  // rotation: the node's slots are known reset only
+        mbar_wait(gate_mbar, gate_parity);     // once the previous pass's barrier is seen
+        reset_ok = true;
+      }
       if (node_hot) {
         ++n_poll;
-        double* child0 = l == 1 ? a.tile_part + ((int64_t)oct * g.M - g.tile0 + (int64_t)j * kFan) * nf
+        double* child0 = l == 1 ? tpart + ((int64_t)oct * g.M - g.tile0 + (int64_t)j * kFan) * nf
                                 : a.node_part[l - 1] + ((int64_t)lo * g.nodes[l - 1] + (int64_t)j * kFan) * nf;
-        if (LOOP) {  // publish, then count it (readers wait for the count after the grid barrier)
-          advance = try_node<NF, false>(child0, nreal, nf, l1_out + ((int64_t)lo * g.nodes[1] + j) * nf);
+        double* out = l1_out + ((int64_t)lo * g.nodes[1] + j) * nf;
+        if (LOOP && l1_reset) {
+          // fence-free (loop kernel, large volumes): the tile partials rotate
+          // (their writers reset them), the level-1 result is published with
+          // relaxed stores into this pass's buffer and the node's slot of the
+          // buffer two passes ahead is reset -- readers poll the results
+          advance = try_node<NF, true, false>(child0, nreal, nf, out);
+          if (advance)
+            for (int f = lane; f < nf; f += 32)
+              st_relaxed(l1_reset + ((int64_t)lo * g.nodes[1] + j) * nf + f, sentinel());
+        } else if (LOOP) {  // publish, then count it (readers wait for the count after the grid barrier)
+          advance = try_node<NF, false>(child0, nreal, nf, out);
           if (advance) {  // (warp-uniform) every lane's sentinel resets, then lane 0's release
             __syncwarp();
             if (lane == 0) red_release_add(&a.ctl->l1_done, 1u);
@@ -305,11 +320,12 @@ __device__ __forceinline__ bool poll_tree32(const double* p, int64_t stride, int
 // further cross-CTA hop is needed.  Each (node, field) pair is one thread's
 // tree32; all kTmaThreads threads call it; scratch is the (idle) stage ring.
 template <int NF>
-__device__ __forceinline__ void loop_upper(const PassArgs& a, const double* l1, double* scratch,
+__device__ __forceinline__ bool loop_upper(const PassArgs& a, const double* l1, double* scratch,
                                            double (*oroot)[NF], double* root, unsigned it = 0,
                                            bool from_tiles = false, double extra_delta = 0.0,
                                            uint32_t upbar = 0u, uint32_t* upphase = nullptr,
-                                           int64_t scratch_doubles = 0, const double* tparts = nullptr) {
+                                           int64_t scratch_doubles = 0, const double* tparts = nullptr,
+                                           bool poll = false) {
   const int tid = threadIdx.x;
   const int nf = 2 * a.c + 2;
   const Geometry& g = a.g;
@@ -352,7 +368,9 @@ __device__ __forceinline__ void loop_upper(const PassArgs& a, const double* l1, 
     l1 = l1s;
   }
   const int ls = from_tiles ? NF : nf;  // row stride of the level-1 results
-  // step 1: level-2 nodes (L == 3) or octant roots (L == 2) from level-1 results
+  // step 1: level-2 nodes (L == 3) or octant roots (L == 2) from level-1
+  // results (fence-free protocol: polled until published)
+  bool ok = true;
   if (g.levels >= 2) {
     for (int pr = tid; pr < g.noct * per * nf; pr += kTmaThreads) {
       const int item = pr / nf, f = pr - item * nf;
@@ -361,11 +379,15 @@ __device__ __forceinline__ void loop_upper(const PassArgs& a, const double* l1, 
       const int nreal = (int64_t)oct * g.M < g.T ? node_real_children(g, oct, 2, k) : 0;
       const double* src = l1 + ((int64_t)lo * g.nodes[1] + (int64_t)k * kFan) * ls + f;
       double r = 0.0;
-      if (nreal) r = from_tiles ? tree32<false>(src, ls, nreal, f == nf - 1) : tree32<true>(src, ls, nreal, f == nf - 1);
+      if (nreal) {
+        if (poll) ok = ok && poll_tree32(src, ls, nreal, f == nf - 1, &r);
+        else r = from_tiles ? tree32<false>(src, ls, nreal, f == nf - 1) : tree32<true>(src, ls, nreal, f == nf - 1);
+      }
       scratch[(int64_t)item * NF + f] = r;
     }
-    __syncthreads();
+    ok = __syncthreads_and(ok) != 0;
     if (tid == 0) probe(a, it, 11, global_ns());
+    if (!ok) return false;
   }
   // step 2: octant roots
   for (int pr = tid; pr < g.noct * nf; pr += kTmaThreads) {
@@ -392,6 +414,7 @@ __device__ __forceinline__ void loop_upper(const PassArgs& a, const double* l1, 
     if (mx) root[f] = fmax(root[f], extra_delta);  // recompute mode: the table delta
   }
   __syncthreads();
+  return true;
 }
 
 // Loop kernel, small volumes (<= kSmallTiles tiles), after the grid barrier
