@@ -6,6 +6,7 @@
 // shard streams and only syncs once per batch to read the device `done` flag
 // (core._iterate's Python loop, core.py:105-132, becomes a device loop).
 #include <dlfcn.h>
+#include <sys/mman.h>
 
 #include <algorithm>
 #include <cmath>
@@ -174,6 +175,11 @@ struct fcm_plan {
   } gkey{};
   Control* host_ctl = nullptr;   // pinned: device -> host reads of the control block
   Control* host_tmpl = nullptr;  // pinned: reset template copied to every shard
+  // pageable host -> device uploads (fcm_upload_pixels / _membership):
+  // kStageThreads host threads, each with its own stream and two pinned slots
+  char* stage_pinned = nullptr;
+  cudaStream_t stage_st[16] = {};
+  cudaEvent_t stage_ev[16][2] = {};
   std::vector<cudaEvent_t> ev_t0, ev_t1;
   cudaEvent_t ev_start = nullptr, ev_pro = nullptr, ev_end = nullptr;
   double t_loop_ms = 0, t_pass_ms = 0, t_pro_ms = 0;
@@ -334,6 +340,14 @@ void release(fcm_plan* p) {
   if (p->ev_end) cudaEventDestroy(p->ev_end);
   if (p->host_ctl) cudaFreeHost(p->host_ctl);
   if (p->host_tmpl) cudaFreeHost(p->host_tmpl);
+  if (p->stage_pinned) {
+    cudaFreeHost(p->stage_pinned);
+    for (int t = 0; t < 16; ++t) {
+      if (p->stage_st[t]) cudaStreamDestroy(p->stage_st[t]);
+      for (int k = 0; k < 2; ++k)
+        if (p->stage_ev[t][k]) cudaEventDestroy(p->stage_ev[t][k]);
+    }
+  }
   drop_graph(p);
   for (int r = 0; r < kOctants; ++r)
     if (p->peer_opened[r]) cudaIpcCloseMemHandle(p->peer_mbox[r]);
@@ -578,6 +592,14 @@ constexpr int kSmallTilesHost = 1024;  // = kSmallTiles (fcm_tma_pipe.cuh): the 
 // ================================================================== C ABI ==
 // host-side row expansion for fcm_download_table (below)
 namespace {
+
+// madvise(MADV_HUGEPAGE) on the 2 MB-aligned interior of [p, p + bytes).
+void advise_huge(void* p, size_t bytes) {
+  if (!p || bytes < ((size_t)4 << 20)) return;
+  const uintptr_t a = ((uintptr_t)p + ((1u << 21) - 1)) & ~(uintptr_t)((1u << 21) - 1);
+  const uintptr_t e = ((uintptr_t)p + bytes) & ~(uintptr_t)((1u << 21) - 1);
+  if (e > a) madvise((void*)a, e - a, MADV_HUGEPAGE);
+}
 
 // SM count of a device, cached (the seam ops size their grids by it).
 int device_sms(int device) {
@@ -846,6 +868,61 @@ int fcm_plan_info(const fcm_plan* p, int64_t* info, int32_t count) {
   return FCM_OK;
 }
 
+// Host -> device copy of `bytes` from a caller buffer.  Pinned (or small)
+// sources go straight to the copy engine; a large pageable source is split
+// over kStageThreads host threads, each copying its range through two 8 MB
+// page-locked slots of the plan (memcpy into one slot while the other's DMA
+// runs on the thread's own stream) -- the driver's own pageable path stages
+// through one buffer on one thread (~11 GB/s here).  Synchronous.
+constexpr int kStageThreads = 16;
+constexpr size_t kStageSlot = (size_t)8 << 20;
+static int h2d_from_host(fcm_plan* p, void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  cudaPointerAttributes at{};
+  const bool pinned = cudaPointerGetAttributes(&at, src) == cudaSuccess && at.type == cudaMemoryTypeHost;
+  cudaGetLastError();
+  int cur = 0;
+  cudaGetDevice(&cur);
+  // (the staging streams live on shard 0's device)
+  if (pinned || bytes < ((size_t)64 << 20) || cur != p->sh[0].device) {
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));
+    return FCM_OK;
+  }
+  if (!p->stage_pinned) {
+    CK(cudaMallocHost(&p->stage_pinned, kStageSlot * 2 * kStageThreads));
+    for (int t = 0; t < kStageThreads; ++t) {
+      CK(cudaStreamCreateWithFlags(&p->stage_st[t], cudaStreamNonBlocking));
+      for (int k = 0; k < 2; ++k) CK(cudaEventCreateWithFlags(&p->stage_ev[t][k], cudaEventDisableTiming));
+    }
+  }
+  CK(cudaStreamSynchronize(st));  // (the destination's earlier users on the plan stream)
+  const int dev = cur;
+  const size_t per = ((bytes + kStageThreads - 1) / kStageThreads + 4095) & ~(size_t)4095;
+  std::vector<char> ok(kStageThreads, 1);
+  auto work = [&](int t) {
+    cudaSetDevice(dev);
+    const size_t b0 = std::min(bytes, t * per), b1 = std::min(bytes, b0 + per);
+    char* slot[2] = {p->stage_pinned + (size_t)(2 * t) * kStageSlot, p->stage_pinned + (size_t)(2 * t + 1) * kStageSlot};
+    int k = 0;
+    for (size_t o = b0; o < b1; o += kStageSlot, k ^= 1) {
+      const size_t len = std::min(kStageSlot, b1 - o);
+      if (cudaEventSynchronize(p->stage_ev[t][k]) != cudaSuccess) ok[t] = 0;  // the slot's last DMA
+      memcpy(slot[k], (const char*)src + o, len);
+      if (cudaMemcpyAsync((char*)dst + o, slot[k], len, cudaMemcpyHostToDevice, p->stage_st[t]) != cudaSuccess ||
+          cudaEventRecord(p->stage_ev[t][k], p->stage_st[t]) != cudaSuccess)
+        ok[t] = 0;
+    }
+    if (cudaStreamSynchronize(p->stage_st[t]) != cudaSuccess) ok[t] = 0;
+  };
+  std::vector<std::thread> th;
+  for (int t = 1; t < kStageThreads; ++t) th.emplace_back(work, t);
+  work(0);
+  for (auto& t : th) t.join();
+  for (char o : ok)
+    if (!o) return fail(p, FCM_E_CUDA, "staged host-to-device copy failed");
+  return FCM_OK;
+}
+
 int fcm_upload_pixels(fcm_plan* p, const void* x) {
   if (check_plan(p) || !x) return FCM_E_ARG;
   const size_t xsz = xkind_bytes(p->xkind);
@@ -855,7 +932,7 @@ int fcm_upload_pixels(fcm_plan* p, const void* x) {
     if (s.g.n_local == 0) continue;
     CK(cudaSetDevice(s.device));
     const char* src = (const char*)x + (s.g.voxel0 - host0) * xsz;
-    CK(cudaMemcpyAsync(s.x, src, s.g.n_local * xsz, cudaMemcpyHostToDevice, s.stream));
+    if (int rc = h2d_from_host(p, s.x, src, s.g.n_local * xsz, s.stream)) return rc;
   }
   for (int i = 0; i < p->nshards; ++i) {
     CK(cudaSetDevice(p->sh[i].device));
@@ -883,8 +960,9 @@ int fcm_upload_membership(fcm_plan* p, const double* u0) {
       int rc = dalloc(p, s, &s.u0_aos, (size_t)s.g.n_local * p->c);
       if (rc) return rc;
     }
-    CK(cudaMemcpyAsync(s.u0_aos, u0 + (s.g.voxel0 - host0) * p->c,
-                       sizeof(double) * s.g.n_local * p->c, cudaMemcpyHostToDevice, s.stream));
+    if (int rc = h2d_from_host(p, s.u0_aos, u0 + (s.g.voxel0 - host0) * p->c,
+                               sizeof(double) * s.g.n_local * p->c, s.stream))
+      return rc;
   }
   for (int i = 0; i < p->nshards; ++i) {
     CK(cudaSetDevice(p->sh[i].device));
@@ -1250,6 +1328,11 @@ int fcm_download_table(fcm_plan* p, const uint8_t* x_host, double* u_out, int32_
   int64_t n = 0;
   for (int i = 0; i < p->nshards; ++i) n += p->sh[i].g.n_local;
   if (u_out || labels_out) {
+    // freshly allocated result arrays (the drop-in returns new arrays every
+    // call) fault in 2 MB pages instead of 4 KB ones where the kernel allows
+    // transparent huge pages on request -- advice only, ignored otherwise
+    advise_huge(u_out, (size_t)n * p->c * sizeof(double));
+    advise_huge(labels_out, (size_t)n * sizeof(int32_t));
     int T = nthreads > 0 ? nthreads : (int)std::thread::hardware_concurrency();
     T = (int)std::max<int64_t>(1, std::min<int64_t>(T, std::max<int64_t>(1, n >> 16)));
     const int64_t chunk = ((n + T - 1) / T + 63) & ~int64_t(63);  // even starts keep the u rows 16-B aligned

@@ -32,7 +32,25 @@ from .types import ClusterCenters, FcmConfig, FcmResult, GrayImage, LabelMap, Me
 C_MAX = 32
 
 
-def pixel_kind(pixels: np.ndarray):
+_scratch = threading.local()
+
+
+def _pinned_scratch(nbytes: int) -> np.ndarray:
+    """This thread's page-locked staging buffer (cudaHostRegister'ed once and
+    reused): run_fcm_gpu narrows float64 pixels straight into it, so the
+    upload runs at pinned-copy speed.  Falls back to pageable memory when
+    registration fails."""
+    buf = getattr(_scratch, "buf", None)
+    if buf is None or buf.nbytes < nbytes:
+        if buf is not None and getattr(_scratch, "pinned", False):
+            lib().fcm_host_unregister(ptr(buf))
+        buf = np.empty(max(nbytes, 1), dtype=np.uint8)
+        _scratch.pinned = lib().fcm_host_register(ptr(buf), buf.nbytes) == _lib.FCM_OK
+        _scratch.buf = buf
+    return buf[:nbytes]
+
+
+def pixel_kind(pixels: np.ndarray, staging: bool = False):
     """Pick the narrowest exact device representation of the pixels.
 
     Integer intensities 0..255 travel and live in HBM as uint8 (every
@@ -40,7 +58,8 @@ def pixel_kind(pixels: np.ndarray):
     imgio.py:102-110); anything else stays float64 (types.py:38-41 accepts
     any finite non-negative value).  float64 input is checked and narrowed in
     one multi-threaded pass in the library (fcm_narrow_pixels).  Returns
-    (FCM_X_*, contiguous array).
+    (FCM_X_*, contiguous array).  staging=True narrows into this thread's
+    pinned staging buffer (valid until the next call; run_fcm_gpu uses it).
     """
     if pixels.dtype == np.uint8:
         return _lib.FCM_X_U8, np.ascontiguousarray(pixels)
@@ -52,7 +71,7 @@ def pixel_kind(pixels: np.ndarray):
     x = np.ascontiguousarray(pixels, dtype=np.float64)
     n = x.shape[0]
     for kind, dt in ((_lib.FCM_X_U8, np.uint8), (_lib.FCM_X_U16, np.uint16)):
-        out = np.empty(n, dtype=dt)
+        out = _pinned_scratch(n * np.dtype(dt).itemsize).view(dt) if staging else np.empty(n, dtype=dt)
         if lib().fcm_narrow_pixels(ptr(x), n, kind, ptr(out), 0) == _lib.FCM_OK:
             return kind, out
     return _lib.FCM_X_F64, x
@@ -355,7 +374,7 @@ def _iterate(x: np.ndarray, u0: np.ndarray | None, cfg: FcmConfig, devices=None,
     (v, u_final, iterations, trace, converged) like the reference.
     """
     _check_c(cfg.c)
-    kind, xx = pixel_kind(np.asarray(x))
+    kind, xx = pixel_kind(np.asarray(x), staging=True)
     n = xx.shape[0]
     if u0 is not None:
         u0 = np.ascontiguousarray(u0, dtype=np.float64)
@@ -394,7 +413,7 @@ def run_fcm_gpu(img: GrayImage, cfg: FcmConfig, devices=None,
     # a PgmImage (imgio.read_pgm_raster) hands its integer raster over as is:
     # 8-bit images reach HBM at 1 B per voxel, 16-bit at 2 B, without a float64 copy
     from .imgio import PgmImage
-    kind, xx = pixel_kind(img.raster if isinstance(img, PgmImage) else img.pixels)
+    kind, xx = pixel_kind(img.raster if isinstance(img, PgmImage) else img.pixels, staging=True)
     plan = FcmPlan(n, cfg.c, kind, devices) if keep_plan else _cached_plan(n, cfg.c, kind, devices)
     try:
         v, trace, k, conv, u, labels, table = _solve(
