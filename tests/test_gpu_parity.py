@@ -502,3 +502,30 @@ def test_label_statistics_need_this_runs_labels():
             plan.label_counts()
         plan.download_table(x, membership=False)
         assert plan.label_counts().sum() == x.shape[0]
+
+
+@pytest.mark.parametrize("c,m", [(8, 1.5), (4, 3.0)])
+def test_intensity_fold_matches_per_voxel_accumulation(c, m):
+    """m != 2 on uint8 pixels: the default intensity-table path regroups the
+    Eq. 3 / objective sums by intensity (exact integer counts x per-intensity
+    terms); FCM_OPT_KERNEL = 3 accumulates them voxel by voxel in fp64.  Same
+    iterations, converged flag and labels; centers and objective trace within
+    1e-12 relative; memberships within 1e-12."""
+    from paper_1601_00072_b200 import _lib
+    x = np.clip(np.rint(mixture_pixels(400_003, c, seed=40 + c)), 0, 255).astype(np.uint8)
+
+    def solve(kernel):
+        with pkg.FcmPlan(x.shape[0], c, _lib.FCM_X_U8) as plan:
+            plan.upload_pixels(x)
+            plan.init_membership(3)
+            plan.set_option(_lib.FCM_OPT_KERNEL, kernel)
+            v, trace, k, conv = plan.run(m, 1e-5, 300)
+            u, lab = plan.download()
+        return v, trace, k, conv, u, lab
+
+    a, b = solve(0), solve(3)
+    assert a[2] == b[2] and a[3] == b[3]
+    assert np.array_equal(a[5], b[5])
+    assert np.allclose(a[0], b[0], rtol=1e-12, atol=0)
+    assert np.allclose(a[1][:a[2]], b[1][:b[2]], rtol=1e-12, atol=0)
+    assert np.abs(a[4] - b[4]).max() <= 1e-12
