@@ -21,6 +21,7 @@
 #include <emmintrin.h>
 
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX3: ranges cost nothing without a tool attached
 
 #include "../../include/fcm_b200.h"
 #include "fcm_kernels.h"
@@ -209,6 +210,18 @@ int fail(fcm_plan* p, int code, const char* fmt, ...) {
       return fail(p, FCM_E_CUDA, "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(e_),      \
                   __FILE__, __LINE__);                                                        \
   } while (0)
+
+// NVTX range for the host-side phases (Nsight Systems / ncu --nvtx timelines):
+// uploads, the solve (prologue, loop-kernel launch, per-pass launches),
+// downloads and the host table expansion.  Per-pass phases
+// inside the persistent loop kernel come from its device timeline
+// (FCM_OPT_PROFILE, tools/pass_phases.py) instead.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 int nf_of(int c) { return 2 * c + 2; }
 
@@ -449,6 +462,9 @@ PassArgs make_args(fcm_plan* p, Shard& s, int seq, double eps, int max_iters) {
 // Launch one prologue (seq == 0) or pass on every shard, then -- when the
 // job has more than one rank -- exchange the roots and finalize everywhere.
 int step(fcm_plan* p, int seq, double eps, int max_iters) {
+  char label[32];
+  snprintf(label, sizeof label, seq == 0 ? "fcm prologue" : "fcm pass %d", seq);
+  NvtxRange nv(label);
   const int nf = nf_of(p->c);
   const bool prologue = seq == 0;
   for (int i = 0; i < p->nshards; ++i) {
@@ -924,6 +940,7 @@ static int h2d_from_host(fcm_plan* p, void* dst, const void* src, size_t bytes, 
 }
 
 int fcm_upload_pixels(fcm_plan* p, const void* x) {
+  NvtxRange nv("fcm_upload_pixels");
   if (check_plan(p) || !x) return FCM_E_ARG;
   const size_t xsz = xkind_bytes(p->xkind);
   const int64_t host0 = p->nranks > p->nshards ? p->sh[0].g.voxel0 : 0;  // rank plans: host buffers hold the rank slice
@@ -950,6 +967,7 @@ int fcm_init_membership(fcm_plan* p, uint64_t seed) {
 }
 
 int fcm_upload_membership(fcm_plan* p, const double* u0) {
+  NvtxRange nv("fcm_upload_membership");
   if (check_plan(p) || !u0) return FCM_E_ARG;
   const int64_t host0 = p->nranks > p->nshards ? p->sh[0].g.voxel0 : 0;  // rank plans: host buffers hold the rank slice
   for (int i = 0; i < p->nshards; ++i) {
@@ -1078,6 +1096,7 @@ static int run_impl(fcm_plan* p, double m, double eps, int32_t max_iters, double
       int share = 0;
       for (int j = 0; j < p->nshards; ++j) share += p->sh[j].device == s.device ? 1 : 0;
       int grid = 0;
+      NvtxRange nv3("fcm loop kernel launch");
       e = launch_loop(p->xkind, p->c, p->mode, a, s.sms, s.stream, &grid, p->variant, p->force_grid, share);
       if (e == cudaSuccess) {
         s.last_grid = grid;
@@ -1202,6 +1221,7 @@ static int run_impl(fcm_plan* p, double m, double eps, int32_t max_iters, double
 // single-shard plans report the failure instead.
 int fcm_run(fcm_plan* p, double m, double eps, int32_t max_iters, double* v_out,
             double* trace_out, int32_t* iterations, int32_t* converged, int32_t* dead_cluster) {
+  NvtxRange nv("fcm_run");
   int rc = run_impl(p, m, eps, max_iters, v_out, trace_out, iterations, converged, dead_cluster);
   if (rc != FCM_OK && rc != FCM_E_DEGENERATE && rc != FCM_E_ARG && p && p->looped_last && p->nshards > 1 &&
       p->nranks == p->nshards && p->host_ctl && (p->host_ctl->dead == -3 || p->host_ctl->dead == -4)) {
@@ -1214,6 +1234,7 @@ int fcm_run(fcm_plan* p, double m, double eps, int32_t max_iters, double* v_out,
 }
 
 int fcm_download(fcm_plan* p, double* u_out, int32_t* labels_out) {
+  NvtxRange nv("fcm_download");
   if (check_plan(p)) return FCM_E_ARG;
   if (!p->run_ok) return fail(p, FCM_E_STATE, "no successful fcm_run to download");
   const int64_t host0 = p->nranks > p->nshards ? p->sh[0].g.voxel0 : 0;  // rank plans: host buffers hold the rank slice
@@ -1266,6 +1287,7 @@ int fcm_download(fcm_plan* p, double* u_out, int32_t* labels_out) {
 
 int fcm_download_table(fcm_plan* p, const uint8_t* x_host, double* u_out, int32_t* labels_out,
                        int32_t nthreads) {
+  NvtxRange nv("fcm_download_table");
   if (check_plan(p)) return FCM_E_ARG;
   if (!p->run_ok) return fail(p, FCM_E_STATE, "no successful fcm_run to download");
   if (p->xkind != XK_U8) return fail(p, FCM_E_ARG, "fcm_download_table needs a uint8 plan");
@@ -1331,6 +1353,7 @@ int fcm_download_table(fcm_plan* p, const uint8_t* x_host, double* u_out, int32_
     // freshly allocated result arrays (the drop-in returns new arrays every
     // call) fault in 2 MB pages instead of 4 KB ones where the kernel allows
     // transparent huge pages on request -- advice only, ignored otherwise
+    NvtxRange nv2("host table expansion");
     advise_huge(u_out, (size_t)n * p->c * sizeof(double));
     advise_huge(labels_out, (size_t)n * sizeof(int32_t));
     int T = nthreads > 0 ? nthreads : (int)std::thread::hardware_concurrency();
