@@ -85,7 +85,10 @@ typedef enum {
   FCM_OPT_PEER_TIMEOUT_MS = 14 /* multi-rank loop kernel: how long a rank waits for a peer's per-pass
                               root before failing fcm_run with FCM_E_NCCL naming the missing rank and
                               pass (default 4000).  Single-process multi-shard plans retry such a
-                              failure with one launch per pass (fcm_last_timing out[6] counts it). */
+                              failure with one launch per pass (fcm_last_timing out[6] counts it). */,
+  FCM_OPT_DEBUG_SOLO_RANK = 15 /* diagnostics: a rank plan runs its slice alone (no root exchange; the
+                              centers are the slice's, not the job's) -- the per-rank pass of an
+                              N-GPU job timed on one GPU (tools/rank_proxy.py) */
 } fcm_option;
 
 typedef struct fcm_plan fcm_plan;

@@ -19,6 +19,7 @@ FCM_X_U8, FCM_X_U16, FCM_X_F64 = 0, 1, 2
 FCM_OPT_BATCH, FCM_OPT_TIMING, FCM_OPT_GRID, FCM_OPT_KERNEL, FCM_OPT_GRAPH = 1, 2, 3, 4, 5
 FCM_OPT_LOOP, FCM_OPT_L2, FCM_OPT_PROFILE, FCM_OPT_SEED_PASS = 6, 7, 8, 9
 FCM_OPT_RECOMPUTE, FCM_OPT_DEBUG_DELAY, FCM_OPT_DEBUG_SHARED_PARTIALS, FCM_OPT_PEER_TIMEOUT_MS = 11, 12, 13, 14
+FCM_OPT_DEBUG_SOLO_RANK = 15
 
 # Every symbol the header declares (tests/test_abi.py checks the .so exports them).
 SIGNATURES = {

@@ -154,6 +154,7 @@ struct fcm_plan {
   int32_t res_tab_l[256] = {};
   unsigned debug_delay_ns = 0;  // loop kernel: one CTA per pass sleeps after the grid barrier (tests)
   int debug_shared_parts = 0;   // loop kernel: single tile-partial buffer (the racy round-1 layout; tests)
+  int solo_rank = 0;            // diagnostics: a rank plan solves its slice without the exchange
   int64_t peer_timeout_ms = 4000;  // loop kernel, multi-rank: how long to wait for a peer's root
   bool force_per_pass = false;  // fcm_run retry after a failed multi-shard loop (shards sharing a device)
   bool looped_last = false;     // the last run_impl ran the loop kernel
@@ -850,6 +851,7 @@ int fcm_set_option(fcm_plan* p, int32_t key, int64_t value) {
       p->debug_delay_ns = (unsigned)value;
       return FCM_OK;
     case FCM_OPT_DEBUG_SHARED_PARTIALS: p->debug_shared_parts = value ? 1 : 0; return FCM_OK;
+    case FCM_OPT_DEBUG_SOLO_RANK: p->solo_rank = value ? 1 : 0; return FCM_OK;
     case FCM_OPT_PEER_TIMEOUT_MS:
       if (value < 0 || value > 3600000) return FCM_E_ARG;
       p->peer_timeout_ms = value;
@@ -1001,7 +1003,7 @@ static int run_impl(fcm_plan* p, double m, double eps, int32_t max_iters, double
   if (max_iters < 1) return fail(p, FCM_E_ARG, "max_iters must be >= 1");
   if (!p->x_ready) return fail(p, FCM_E_STATE, "fcm_upload_pixels has not been called");
   if (!p->init_src) return fail(p, FCM_E_STATE, "no initial membership (init or upload)");
-  if (p->nshards == 1 && p->nranks > 1 && !p->use_nccl && !p->p2p_ready)
+  if (p->nshards == 1 && p->nranks > 1 && !p->use_nccl && !p->p2p_ready && !p->solo_rank)
     return fail(p, FCM_E_STATE, "rank plan without NCCL: call fcm_connect_peers first");
   set_powers(p, m);
 
@@ -1052,9 +1054,13 @@ static int run_impl(fcm_plan* p, double m, double eps, int32_t max_iters, double
     // SplitMix64-bound work at 4 CTAs per SM instead of the loop kernel's 2
     // (C4: 0.75 vs 0.84 ms; same v_1 bit for bit); recompute mode needs the
     // in-loop pass 0 (it records the intensities present)
+    // (the prologue kernel's root meets the other shards' only through the
+    // per-pass exchange machinery: multi-shard and multi-rank plans keep the
+    // seeded start inside the loop kernel, whose pass 0 exchanges like any pass)
     const bool small = p->sh[0].g.tiles_local <= kSmallTilesHost;
+    const bool alone = p->nshards == 1 && p->nranks == 1;
     const bool seed_pass = p->init_src == 1 &&
-                           (p->seed_pass == 1 || (p->seed_pass == 2 && (small || p->recompute)));
+                           (p->seed_pass == 1 || (p->seed_pass == 2 && (small || p->recompute || !alone)));
     if (!seed_pass && (rc = step(p, 0, eps, max_iters))) return rc;
     for (int i = 1; i < p->nshards; ++i) {  // shards start together with shard 0
       CK(cudaSetDevice(p->sh[i].device));
@@ -1072,8 +1078,8 @@ static int run_impl(fcm_plan* p, double m, double eps, int32_t max_iters, double
       // recompute needs the intensity set, tracked by the seeded pass 0
       a.recompute = (p->recompute && seed_pass && p->xkind == XK_U8 && p->mode == MODE_M2 && p->c <= 8 &&
                      p->variant == 0) ? 1 : 0;
-      a.mb_ranks = p->nranks;
-      a.mb_rank = p->nshards > 1 ? i : p->rank;
+      a.mb_ranks = p->solo_rank ? 1 : p->nranks;
+      a.mb_rank = p->solo_rank ? 0 : (p->nshards > 1 ? i : p->rank);
       a.mb_run = run ? run : 1;
       a.mbox_local = s.mbox;
       for (int r = 0; r < p->nranks; ++r) a.mbox_peer[r] = p->nshards > 1 ? p->sh[r].mbox : p->peer_mbox[r];

@@ -15,13 +15,19 @@ from conftest import REPO
 pytestmark = pytest.mark.gpu
 
 
-def test_two_process_mailbox_exchange_bitwise():
+@pytest.mark.parametrize("n", [300_007, 20_000_003])
+def test_two_process_mailbox_exchange_bitwise(n):
+    """300 K voxels: every CTA reduces the tile partials (small-volume pass
+    end); 20 M voxels: 1,221 tiles per rank, level-1 owners and the
+    seeded start inside each rank's loop kernel (pass 0 exchanges its root
+    like every pass)."""
     out = os.path.join(REPO, "gpurun_out", "ipc_two_ranks.txt")
     os.makedirs(os.path.dirname(out), exist_ok=True)
     if os.path.exists(out):
         os.remove(out)
+    env = dict(os.environ, FCM_IPC_N=str(n))
     r = subprocess.run([sys.executable, os.path.join(REPO, "tools", "ipc_two_ranks.py"), "--same-gpu"],
-                       capture_output=True, text=True, timeout=240)
+                       capture_output=True, text=True, timeout=400, env=env)
     assert r.returncode == 0, r.stderr[-2000:]
     assert open(out).read().startswith("OK"), open(out).read()
 

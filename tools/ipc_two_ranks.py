@@ -32,7 +32,7 @@ def worker(rank, world, port, same_gpu, out, stuck=-1, kill=-1):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    n = 300_007
+    n = int(os.environ.get("FCM_IPC_N", "300007"))  # (> 8.4 M voxels: >1024 tiles per rank, owner path)
     x = np.clip(np.rint(mixture_pixels(n, 3, seed=9)), 0, 255).astype(np.uint8)
     dev = 0 if same_gpu else rank
     plan = pkg.FcmPlan.for_rank(n, 3, _lib.FCM_X_U8, dev, world, rank, None)
