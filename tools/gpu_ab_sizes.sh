@@ -12,3 +12,7 @@ import json; d=json.load(open('gpurun_out/ab_${v}_${cfg}_$r.json')); print('$v $
   done
   timeout 300 python tools/pass_phases.py C3@16777216 C3@1000000 C1 --warm 5 2>&1 | grep -E "^C" | sed "s/^/$v run$r /"
 done; done
+for v in A B; do
+  if [ $v = A ]; then export FCM_B200_LIB=$A; else unset FCM_B200_LIB; fi
+  timeout 600 python tools/rank_proxy.py 2>&1 | grep -E "^ 8 " | sed "s/^/$v rank8 /"
+done
