@@ -612,7 +612,8 @@ namespace {
 
 // madvise(MADV_HUGEPAGE) on the 2 MB-aligned interior of [p, p + bytes).
 void advise_huge(void* p, size_t bytes) {
-  if (!p || bytes < ((size_t)4 << 20)) return;
+  static const bool off = getenv("FCM_NO_HUGEPAGE") != nullptr;  // A/B switch (diagnostics)
+  if (off || !p || bytes < ((size_t)4 << 20)) return;
   const uintptr_t a = ((uintptr_t)p + ((1u << 21) - 1)) & ~(uintptr_t)((1u << 21) - 1);
   const uintptr_t e = ((uintptr_t)p + bytes) & ~(uintptr_t)((1u << 21) - 1);
   if (e > a) madvise((void*)a, e - a, MADV_HUGEPAGE);

@@ -26,3 +26,5 @@ import json,sys; d=json.load(open('gpurun_out/bench_$f.json')); print('$f', d.ge
 grep -E "^C|solve|next" gpurun_out/pass_phases.txt
 cat gpurun_out/exchange_C2.txt gpurun_out/exchange_C4.txt
 ls gpurun_out/parity
+timeout 600 python tools/rank_proxy.py --exchange-us 2.4,2.3,3.5 > gpurun_out/rank_proxy.txt 2>&1; tail -9 gpurun_out/rank_proxy.txt
+timeout 900 python tools/e2e_phases.py > gpurun_out/e2e_phases.txt 2>&1; tail -10 gpurun_out/e2e_phases.txt
