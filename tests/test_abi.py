@@ -92,3 +92,20 @@ def test_product_path_does_not_import_oracle():
             "import paper_1601_00072_b200.engine; "
             "bad=[m for m in sys.modules if m.startswith('oracle')]; assert not bad, bad") % REPO
     subprocess.run([sys.executable, "-c", code], check=True)
+
+
+def test_pixel_kind_staging_buffer():
+    """run_fcm_gpu / _iterate narrow float64 pixels into this thread's reused
+    staging buffer (page-locked when a GPU is present, pageable otherwise):
+    same kind and values as a fresh array, and the buffer is reused, not
+    reallocated, for a same-size or smaller image."""
+    from paper_1601_00072_b200 import engine
+    rng = np.random.default_rng(3)
+    x = rng.integers(0, 256, 1_000_003).astype(np.float64)
+    k0, a0 = pkg.pixel_kind(x)
+    k1, a1 = engine.pixel_kind(x, staging=True)
+    assert k0 == k1 == _lib.FCM_X_U8 and np.array_equal(a0, a1)
+    base = engine._scratch.buf
+    k2, a2 = engine.pixel_kind(x[:500_000] * 200.0, staging=True)  # 16-bit values now
+    assert k2 == _lib.FCM_X_U16 and np.array_equal(a2, (x[:500_000] * 200).astype(np.uint16))
+    assert engine._scratch.buf is base
