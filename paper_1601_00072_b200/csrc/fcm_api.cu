@@ -908,7 +908,13 @@ static int h2d_from_host(fcm_plan* p, void* dst, const void* src, size_t bytes, 
     return FCM_OK;
   }
   if (!p->stage_pinned) {
-    CK(cudaMallocHost(&p->stage_pinned, kStageSlot * 2 * kStageThreads));
+    if (cudaMallocHost(&p->stage_pinned, kStageSlot * 2 * kStageThreads) != cudaSuccess) {
+      cudaGetLastError();  // no page-locked memory to spare: the driver's own pageable path
+      p->stage_pinned = nullptr;
+      CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+      CK(cudaStreamSynchronize(st));
+      return FCM_OK;
+    }
     for (int t = 0; t < kStageThreads; ++t) {
       CK(cudaStreamCreateWithFlags(&p->stage_st[t], cudaStreamNonBlocking));
       for (int k = 0; k < 2; ++k) CK(cudaEventCreateWithFlags(&p->stage_ev[t][k], cudaEventDisableTiming));
