@@ -106,3 +106,23 @@ def test_tile_size_rule(n, tile):
     g = geometry(n)
     assert g["tile"] == tile
     assert g["T"] <= 64 * 296 or tile == 1024
+
+
+import pytest  # noqa: E402
+
+
+@pytest.mark.parametrize("m", [5, 7, 9, 13, 17, 33, 65])
+def test_butterfly_is_one_stride_tree_per_field(m):
+    """The consumer warps' tile-end butterfly (fcm_device.cuh::bfly_level,
+    restated in tree_model.bfly_reduce) leaves every field on exactly one lane,
+    and each field's value is exactly the stride tree over its 32 lane values
+    -- one fixed shape whichever lane adds, for every field count the kernels
+    instantiate (2c+1 sum fields, c = 2..32)."""
+    import random
+    from tree_model import bfly_reduce, stride_tree
+    rnd = random.Random(m)
+    lanes = [[rnd.uniform(0, 1) * 2.0 ** rnd.randint(-30, 30) for _ in range(m)] for _ in range(32)]
+    got = bfly_reduce(lanes)
+    assert sorted(got) == list(range(m))
+    for f in range(m):
+        assert got[f] == stride_tree([lanes[i][f] for i in range(32)])

@@ -1,6 +1,6 @@
 """Python restatement of the device reduction tree (test helper).
 
-Mirrors fcm_device.cuh::warp_tree and fcm_kernels.cuh::tile_finish /
+Mirrors fcm_device.cuh::warp_tree, bfly_level (the tile-internal lane tree) and fcm_kernels.cuh::tile_finish /
 fcm_dispatch.cu::finalize_kernel so the CPU suite can prove, without a GPU,
 that the tree shape makes the global root independent of the rank count.
 """
@@ -59,3 +59,55 @@ def combine_ranks(roots):
     roots = np.asarray(roots)
     nf = roots.shape[1]
     return np.array([warp_tree(list(roots[:, f]), f == nf - 1) for f in range(nf)])
+
+
+def bfly_reduce(lanes):
+    """Python restatement of fcm_device.cuh::bfly_level / bfly_field: lanes is
+    a list of 32 lists of M field values.  Returns {field: value} as the
+    lanes hold them after the five halving levels."""
+    m = len(lanes[0])
+    v = [list(x) for x in lanes]
+    size = m
+    for s in (16, 8, 4, 2, 1):
+        h = (size + 1) // 2
+        nv = []
+        for lane in range(32):
+            hi = bool(lane & s)
+            partner = lane ^ s
+            cur = []
+            for k in range(h):
+                a = v[lane][k]
+                b = v[lane][h + k] if h + k < size else 0.0
+                pa = v[partner][k]
+                pb = v[partner][h + k] if h + k < size else 0.0
+                keep = b if hi else a
+                recv = pb if hi else pa  # the partner gives the half this lane keeps
+                cur.append(keep + recv)
+            nv.append(cur)
+        v = nv
+        size = h
+    out = {}
+    for lane in range(32):
+        off, mm, real = 0, m, m
+        for s in (16, 8, 4, 2, 1):
+            h = (mm + 1) // 2
+            if lane & s:
+                off += h
+                real = max(real - h, 0)
+            else:
+                real = min(real, h)
+            mm = h
+        for k in range(size):
+            if k < real:
+                assert off + k not in out, "two lanes hold one field"
+                out[off + k] = v[lane][k]
+    return out
+
+
+def stride_tree(vals):
+    """The tile-internal lane tree the butterfly evaluates: level 1 pairs lanes
+    i and i ^ 16, level 2 the results of i and i ^ 8, ...."""
+    x = list(vals)
+    for s in (16, 8, 4, 2, 1):
+        x = [x[i] + x[i + s] for i in range(s)]  # lane i < s keeps i, partner i + s
+    return x[0]
