@@ -489,8 +489,10 @@ def run_ours(args, rank, world, local_rank, dist):
             + "<uint8_t,%d,%s>" % (c, ("MODE_LUT2" if args.kernel == "tma" else "MODE_M2")
                                    if m == 2.0 and args.kernel in ("tma", "direct")
                                    else ("MODE_LUT" if args.kernel in ("tma", "lut") else "MODE_GEN")),
-            "timing": ("CUDA events around the persistent loop kernel (one launch = every pass of a solve, grid "
-                       "barriers included) on its launching stream, timed region" if looped else
+            "timing": ("CUDA events around the persistent loop kernel (one launch = every pass of a solve, the "
+                       "pass ends included; the seeded start too when it runs as pass 0, else in the prologue "
+                       "kernel outside this launch and its bytes outside 'achieved') on its launching stream, "
+                       "timed region" if looped else
                        "pass kernels timed one by one with CUDA events (FCM_OPT_TIMING) after the timed region"),
         },
         "e2e": {
