@@ -615,8 +615,12 @@ cudaError_t launch_loop_c(int xkind, int mode, const PassArgs& a, int sms, cudaS
     if (xkind == XK_U8) {
       if (C <= 8 && variant != 3 && (variant == 2 || !m2))
         return launch_loop_tma<uint8_t, C, (C <= 8 ? MODE_LUT : MODE_GEN)>(a, sms, st, grid_out, force_grid, share);
-      if (C <= 8 && m2 && variant == 0)
-        return launch_loop_tma<uint8_t, C, (C <= 8 ? MODE_LUT2 : MODE_GEN)>(a, sms, st, grid_out, force_grid, share);
+      if (C <= 8 && m2 && variant == 0)  // large volumes: the prefetching instantiation
+        return a.g.tiles_local > kSmallTiles
+                   ? launch_loop_tma<uint8_t, C, (C <= 8 ? MODE_LUT2 : MODE_GEN), true>(a, sms, st, grid_out,
+                                                                                       force_grid, share)
+                   : launch_loop_tma<uint8_t, C, (C <= 8 ? MODE_LUT2 : MODE_GEN)>(a, sms, st, grid_out, force_grid,
+                                                                                 share);
       return m2 ? launch_loop_tma<uint8_t, C, MD>(a, sms, st, grid_out, force_grid, share)
                 : launch_loop_tma<uint8_t, C, MODE_GEN>(a, sms, st, grid_out, force_grid, share);
     }

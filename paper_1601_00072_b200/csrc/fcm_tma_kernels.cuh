@@ -33,7 +33,7 @@ __device__ __forceinline__ void tma_init_barriers(uint8_t* smem, RedSlots<2 * C 
   const uint32_t bar0 = smem_u32(smem + L::kBarOff);
   for (int s = 0; s < L::kStages; ++s) {
     mbar_init(bar0 + 8u * s, 1);
-    mbar_init(bar0 + 8u * (L::kStages + s), kWarps);
+    mbar_init(bar0 + 8u * (L::kStages + s), kThreads);
   }
   for (int s = 0; s < kSlots; ++s) {
     mbar_init(smem_u32(&rs.full[s]), kThreads);
@@ -100,7 +100,11 @@ __global__ void __launch_bounds__(kTmaThreads, 2) pass_tma_kernel(PassArgs a) {
 // passes; the CTA that completes a pass's reduction tree finalizes v_{k+1}
 // and the stop test before it arrives.  u is updated in place.  No
 // per-iteration launch, no host round trip, ring barriers initialised once.
-template <typename XT, int C, int MODE>
+// PF (large volumes, uint8 tables): the next pass's static tile is issued at
+// the pass end (prefetch_static) and the post-pass scratch lives in the
+// table region; a separate instantiation, so the small-volume kernel keeps
+// its register allocation (same-box A/B, profiles/ab_r02/variants.txt).
+template <typename XT, int C, int MODE, bool PF = false>
 __global__ void __launch_bounds__(kTmaThreads, 2) loop_tma_kernel(PassArgs a) {
   constexpr bool LUT = MODE == MODE_LUT;
   constexpr int NF = 2 * C + 2;
@@ -152,6 +156,11 @@ __global__ void __launch_bounds__(kTmaThreads, 2) loop_tma_kernel(PassArgs a) {
   // at the grid barrier and polls the level-1 results for the levels above
   const bool proto_l = !from_tiles && !a.debug_shared_parts;
   const bool proto = proto_s || proto_l;
+  // PF: prefetch only when the owner path runs and its scratch fits the table region
+  const bool pf = PF && proto_l &&
+                  (int64_t)a.g.noct * (a.g.levels == 3 ? a.g.nodes[2] : 1) * NF * 8 <= (int64_t)L::kLutBytes;
+  int pre = 0;  // producer: chunks of this pass's static tile already issued
+  Pipe pfp;     // producer: ring position of the last prefetch (drained at exit)
   const int64_t tlen = (int64_t)a.g.tiles_local * (2 * a.c + 2);
   // recompute mode (SURVEY 8(d) "effective"): passes >= 2 stream x only;
   // u_{k-1} is never read back -- delta_k = max over the intensities present
@@ -194,7 +203,8 @@ __global__ void __launch_bounds__(kTmaThreads, 2) loop_tma_kernel(PassArgs a) {
         fence_proxy_async_global();
         const ProduceGate gate{&a.ctl->bar_count, (gnext - 1u) * gridDim.x, smem_u32(&gatebar)};
         const int n = tma_produce<XT, C, MODE>(a, smem, ps, &a.ctl->tile_next[1], it, it == 0 || (recomp && it >= 2),
-                                                     sched, true, proto ? &gate : nullptr);
+                                                     sched, true, proto ? &gate : nullptr, pre);
+        pre = 0;
         if (n < 0) {
           a.ctl->dead = -3;  // a stuck CTA (cannot happen with co-resident CTAs): flag the run
           a.ctl->done = 1;
@@ -215,6 +225,11 @@ __global__ void __launch_bounds__(kTmaThreads, 2) loop_tma_kernel(PassArgs a) {
         if ((tid & 31) == 0) probe(a, it, 7, global_ns());
       } else {
         bar_sync_end();
+        if (PF && pf && it < (unsigned)a.max_iters) {  // the producer warp (drained at exit if unused)
+          pfp = ps;
+          const int n = prefetch_static<XT, C, MODE>(a, smem, ps, recomp && it + 1u >= 2u);
+          if (tid == kProducerTid) pre = n;
+        }
       }
     } else {
       if (it == 0) {
@@ -286,8 +301,8 @@ __global__ void __launch_bounds__(kTmaThreads, 2) loop_tma_kernel(PassArgs a) {
         __syncthreads();
       }
       const double xdelta = (recomp && it >= 2) ? sdelta : 0.0;
-      const bool ok = loop_upper<NF>(a, l1, reinterpret_cast<double*>(smem), oroot, rs.root, it, false, xdelta,
-                                     0u, &upphase, L::kRingBytes / 8, nullptr, true);
+      const bool ok = loop_upper<NF>(a, l1, reinterpret_cast<double*>(smem + (PF && pf ? L::kLutOff : 0)), oroot,
+                                     rs.root, it, false, xdelta, 0u, &upphase, L::kRingBytes / 8, nullptr, true);
       if (!ok || s_abort) {
         if (tid == 0) {
           a.ctl->dead = -3;
@@ -334,6 +349,15 @@ __global__ void __launch_bounds__(kTmaThreads, 2) loop_tma_kernel(PassArgs a) {
     if (loop_decide(a, rs.root, it)) break;
     if (tid == 0) probe(a, it, 14, global_ns());
   }
+  // a prefetch for a pass that never ran: its bulk copies must land before
+  // the CTA's shared memory goes away
+  if (PF && tid == kProducerTid && pre > 0) {
+    const uint32_t bar0 = smem_u32(smem + L::kBarOff);
+    for (int k = 0; k < pre; ++k) {
+      mbar_wait(bar0 + 8u * pfp.stage, pfp.phase);
+      pfp.advance<L::kStages>();
+    }
+  }
   // (the scheduler counter and the barrier count are reset by fcm_run's
   // control-block upload before the next launch)
 }
@@ -364,11 +388,11 @@ inline cudaError_t launch_pass_tma(const PassArgs& a, int sms, cudaStream_t st, 
 
 // The persistent loop kernel needs every CTA resident at once: cooperative
 // launch (fails instead of deadlocking when the grid cannot be co-resident).
-template <typename XT, int C, int MODE>
+template <typename XT, int C, int MODE, bool PF = false>
 inline cudaError_t launch_loop_tma(const PassArgs& a, int sms, cudaStream_t st, int* grid_out,
                                    int force_grid, int share = 1) {
   using L = TmaLayout<XT, C, MODE>;
-  auto k = loop_tma_kernel<XT, C, MODE>;
+  auto k = loop_tma_kernel<XT, C, MODE, PF>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kSmemBytes);
   if (e != cudaSuccess) return e;
   int per_sm = 0;

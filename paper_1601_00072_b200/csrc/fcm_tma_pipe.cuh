@@ -374,10 +374,67 @@ struct ProduceGate {
 };
 __device__ __forceinline__ bool wait_count(unsigned* ctr, unsigned target);
 
+// Large-volume loop kernel (loop_tma_kernel<..., PF = true>): as soon as
+// this CTA's own stream is done (after the pass-end CTA barrier, which orders
+// the consumers' u_k stores before this warp; the proxy fence hands them to
+// the bulk copies) the producer warp issues the first stages of the NEXT
+// pass's static tile b -- data this CTA wrote itself -- so they land while
+// the root is polled and the next table is built.  Lane k issues chunk k into
+// ring stage (stage + k); lane 0 owns the pipe position.  Returns the chunks
+// issued.
+template <typename XT, int C, int MODE>
+__device__ __forceinline__ int prefetch_static(const PassArgs& a, uint8_t* smem, Pipe& ps, bool x_only) {
+  using L = TmaLayout<XT, C, MODE>;
+  constexpr int S = L::kStages;
+  const int lane = threadIdx.x & 31;
+  const uint32_t bar0 = smem_u32(smem + L::kBarOff);
+  StageMeta* meta = reinterpret_cast<StageMeta*>(smem + L::kMetaOff);
+  const bool keep = a.keep_l2 != 0;
+  const uint64_t pol = keep ? l2_keep_policy() : 0ull;
+  const int c = C <= 8 ? C : a.c;
+  const int lt = (int)blockIdx.x;
+  const int64_t tile = int64_t(1) << a.g.tile_shift;
+  const int64_t nch64 = (a.g.n_local - (int64_t)lt * tile + kChunk - 1) / kChunk;
+  const int per = (int)(tile / kChunk);
+  const int nch = nch64 < per ? (int)nch64 : per;
+  const int pre = nch < S ? nch : S;
+  const int st0 = __shfl_sync(0xffffffffu, ps.stage, 0);
+  const uint32_t ph0 = __shfl_sync(0xffffffffu, ps.phase, 0);
+  fence_proxy_async_global();
+  if (lane < pre) {
+    const int stg = (st0 + lane) % S;
+    const uint32_t ph = ph0 ^ (uint32_t)(((st0 + lane) / S) & 1);
+    mbar_wait(bar0 + 8u * (S + stg), ph ^ 1u);
+    meta[stg].tile = lt;
+    meta[stg].chunk = lane;
+    meta[stg].last = lane == nch - 1;
+    const uint32_t fb = bar0 + 8u * stg;
+    mbar_arrive_tx(fb, (uint32_t)(L::kXBytes + (x_only ? 0 : c * L::kUBytes)));
+    const int64_t i0 = (int64_t)lt * tile + (int64_t)lane * kChunk;
+    uint8_t* sp = smem + stg * L::kStageBytes;
+    const void* xs = reinterpret_cast<const XT*>(a.x) + i0;
+    if (keep) bulk_g2s_keep(smem_u32(sp), xs, L::kXBytes, fb, pol);
+    else bulk_g2s(smem_u32(sp), xs, L::kXBytes, fb);
+#pragma unroll
+    for (int j = 0; j < C; ++j)
+      if (j < c && !x_only) {
+        const uint32_t dst = smem_u32(sp + L::kXBytes + j * L::kUBytes);
+        const float* src = a.u_cur + j * a.g.plane + i0;
+        if (keep) bulk_g2s_keep(dst, src, L::kUBytes, fb, pol);
+        else bulk_g2s(dst, src, L::kUBytes, fb);
+      }
+  }
+  if (lane == 0)
+    for (int k = 0; k < pre; ++k) ps.advance<S>();
+  __syncwarp();
+  return pre;
+}
+
 template <typename XT, int C, int MODE>
 __device__ __forceinline__ int tma_produce(const PassArgs& a, uint8_t* smem, Pipe& ps, unsigned* counter,
                                            unsigned it = 0, bool x_only = false, unsigned base = 0,
-                                           bool first_static = false, const ProduceGate* gate = nullptr) {
+                                           bool first_static = false, const ProduceGate* gate = nullptr,
+                                           int pre = 0) {
   using L = TmaLayout<XT, C, MODE>;
   constexpr int S = L::kStages;
   const uint32_t bar0 = smem_u32(smem + L::kBarOff);
@@ -419,7 +476,8 @@ __device__ __forceinline__ int tma_produce(const PassArgs& a, uint8_t* smem, Pip
     const int64_t left = a.g.n_local - base;
     const int64_t nch64 = (left + kChunk - 1) / kChunk;
     const int nch = nch64 < chunks_per_tile ? (int)nch64 : chunks_per_tile;
-    for (int ch = 0; ch < nch; ++ch) {
+    // (the static tile's first `pre` chunks went out at the end of the last pass)
+    for (int ch = (first_static && claimed == 1) ? pre : 0; ch < nch; ++ch) {
       mbar_wait(bar0 + 8u * (S + ps.stage), ps.phase ^ 1u);
       meta[ps.stage].tile = lt;
       meta[ps.stage].chunk = ch;
@@ -542,8 +600,7 @@ __device__ __forceinline__ void tma_consume_seed(const PassArgs& a, uint8_t* sme
     const StageMeta mt = meta[ps.stage];
     const uint8_t* st = smem + ps.stage * L::kStageBytes;
     if (mt.tile < 0) {
-      __syncwarp();
-      if ((tid & 31) == 0) mbar_arrive(bar0 + 8u * (S + ps.stage));
+      mbar_arrive(bar0 + 8u * (S + ps.stage));  // every consumer thread (count kThreads)
       ps.advance<S>();
       if (track) {
 #pragma unroll
@@ -588,8 +645,7 @@ __device__ __forceinline__ void tma_consume_seed(const PassArgs& a, uint8_t* sme
       xd[2] = p1.x;
       xd[3] = p1.y;
     }
-    __syncwarp();
-    if ((tid & 31) == 0) mbar_arrive(bar0 + 8u * (S + ps.stage));
+    mbar_arrive(bar0 + 8u * (S + ps.stage));  // every consumer thread (count kThreads)
     ps.advance<S>();
     float4 un[C];
     seed_quad<C, MODE>(a, pw, c, i0, xd, a.g.n_local - i0, un, acc);
@@ -658,8 +714,7 @@ __device__ __forceinline__ void tma_consume(const PassArgs& a, uint8_t* smem, Pi
     const uint8_t* st = smem + ps.stage * L::kStageBytes;
     if (mt.tile < 0) {
       if (it && tid == 0) probe(a, it, 19, global_ns());
-      __syncwarp();
-      if ((tid & 31) == 0) mbar_arrive(bar0 + 8u * (S + ps.stage));
+      mbar_arrive(bar0 + 8u * (S + ps.stage));  // every consumer thread (count kThreads)
       ps.advance<S>();
       // end-of-pass slot for the reducer
       mbar_wait(smem_u32(&rs.empty[sp.stage]), sp.phase ^ 1u);
@@ -696,8 +751,7 @@ __device__ __forceinline__ void tma_consume(const PassArgs& a, uint8_t* smem, Pi
       uo[j] = make_float4(0.f, 0.f, 0.f, 0.f);
       if (j < c && !XONLY) uo[j] = *reinterpret_cast<const float4*>(st + L::kXBytes + j * L::kUBytes + tid * 16);
     }
-    __syncwarp();
-    if ((tid & 31) == 0) mbar_arrive(bar0 + 8u * (S + ps.stage));
+    mbar_arrive(bar0 + 8u * (S + ps.stage));  // every consumer thread (count kThreads)
     ps.advance<S>();
     float4 un[C];
 #pragma unroll

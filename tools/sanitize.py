@@ -1,5 +1,7 @@
 """Small solves for compute-sanitizer (memcheck / synccheck / racecheck /
-initcheck): the C1 slice through every launch mode the product uses.
+initcheck): the C1 slice through every launch mode the product uses, and
+one volume above kSmallTiles (the owner-path loop kernel that prefetches the
+next pass's static tile, stopped by max_iters with a prefetch in flight).
 
     compute-sanitizer --tool memcheck python tools/sanitize.py
 
@@ -27,7 +29,7 @@ n = x8.shape[0]
 def case(name, kind=_lib.FCM_X_U8, x=x8, c=3, m=2.0, devices=None, opts=(), table=True, max_iters=500):
     if only and name not in only:
         return
-    with pkg.FcmPlan(n, c, kind, devices) as plan:
+    with pkg.FcmPlan(x.shape[0], c, kind, devices) as plan:
         plan.upload_pixels(x)
         plan.init_membership(0)
         for k, v in opts:
@@ -53,3 +55,5 @@ case("shards4", devices=[0, 0, 0, 0], opts=((_lib.FCM_OPT_PEER_TIMEOUT_MS, 2000)
 case("u16", kind=_lib.FCM_X_U16, x=(x8.astype(np.uint16) * 200))
 case("f64", kind=_lib.FCM_X_F64, x=x8.astype(np.float64) + 0.5)
 case("c20", c=20, max_iters=30)
+if only and "large_owner" in only:  # (not in the default list: minutes under memcheck)
+    case("large_owner", x=make_config("C3@9000000"), max_iters=3)
