@@ -10,7 +10,7 @@ timeout 900 python bench.py > gpurun_out/bench_C4.json 2> gpurun_out/bench_C4.er
 timeout 900 python bench.py --impl reference --steps 5 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
 timeout 600 python bench.py --config C2 --no-cpu-baseline > gpurun_out/bench_C2.json 2> gpurun_out/bench_C2.err
 timeout 900 python bench.py --config C5 --no-cpu-baseline --steps 3 > gpurun_out/bench_C5.json 2> gpurun_out/bench_C5.err
-timeout 300 python tools/pass_phases.py C1 C3@1000000 C2 > gpurun_out/pass_phases.txt 2>&1
+timeout 600 python tools/pass_phases.py C1 C3@1000000 C2 C3@16777216 > gpurun_out/pass_phases.txt 2>&1
 timeout 600 python tools/exchange_latency.py C2 > gpurun_out/exchange_C2.txt 2>&1
 timeout 600 python tools/exchange_latency.py C4 > gpurun_out/exchange_C4.txt 2>&1
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
